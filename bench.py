@@ -1,0 +1,417 @@
+#!/usr/bin/env python3
+"""PagedEviction hot-path benchmark (BASELINE.json metric):
+
+    eviction step HBM GB/s (% of peak); p50 evict-step µs; pruned decode tokens/s
+
+Workload (N=1 line): BASELINE config 3 — Llama-3.1-8B KV geometry (32 layers,
+8 KV heads, head_dim 128, 32 query heads), batch 64, 32K-token prompts,
+budget C=4096, page size B=16, bf16, PER_KV_HEAD tables (16384 per GPU).
+Weak scaling: every rank holds its own 64 sequences (own pool, tables and
+free list; no data-path collective), NCCL only for the max-over-ranks time.
+
+Setup (untimed, but measured with CUDA events and reported under
+"prefill"): K1 prefill prune+pack of every layer from synthetic N(0,1) K/V.
+
+One bench STEP = one eviction cycle of the whole batch: B=16 decode tokens
+appended to every table (K0, one launch per token over all layers) followed
+by the PagedEviction block eviction of every table (K2, one launch per
+layer, pages rescored from their resident K/V bytes). `value` = algorithmic
+bytes of the step (K2: (C+B)*row + 8*(C/B+1) + 4 per table; K0: 2*row+4
+per table per token) / device time of the step, all ranks.
+
+`e2e`: the same cycle through the C-ABI with HOST buffers: every token's
+K/V rows are copied from pinned host memory inside the timed region and the
+victims are read back to host after every eviction launch.
+
+`--impl reference`: the reference's own CPU implementation (oracle/_ref,
+compiled from the reference sources) on the same config, all host threads,
+on a bounded sample of tables.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "eviction step HBM GB/s (% of peak); p50 evict-step µs; pruned decode tokens/s"
+
+CONFIGS = {
+    # name: (layers, kv_heads, head_dim, q_heads, seqs, prompt, budget, dtype)
+    "cfg1": dict(layers=16, kvh=8, d=64, qh=32, seqs=1, L=4096, C=1024, dtype="f32",
+                 desc="Llama-3.2-1B KV geometry, 1 seq, 4K fp32 prefill, C=1024"),
+    "cfg2": dict(layers=28, kvh=8, d=128, qh=24, seqs=32, L=16384, C=2048, dtype="bf16",
+                 desc="Llama-3.2-3B KV geometry, batch 32, 16K context, C=2048, bf16"),
+    "cfg3": dict(layers=32, kvh=8, d=128, qh=32, seqs=64, L=32768, C=4096, dtype="bf16",
+                 desc="Llama-3.1-8B KV geometry, batch 64, 32K context, C=4096, bf16"),
+}
+B = 16
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- helpers
+def k2_bytes_per_table(C, row):
+    return (C + B) * row + 8 * (C // B + 1) + 4
+
+
+def k1_bytes_per_table(L, C, row):
+    keep = min(L, C)
+    return L * row + keep * row + 4 * keep + 4 * ((keep + B - 1) // B)
+
+
+def k3_bytes_per_table(R, row, G, d, q_elt):
+    return R * row + 4 * ((R + B - 1) // B) + G * d * (q_elt + 4)
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    import oracle
+
+    ref = oracle.Reference()
+    threads = os.cpu_count() or 1
+    row = 2 * cfg["d"] * 4  # the reference stores float32 K and V
+    row_alg = 2 * cfg["d"] * (2 if cfg["dtype"] == "bf16" else 4)
+    C = cfg["C"]
+    # bounded sample: `tables` tables per step, one eviction cycle each
+    tables = args.ref_tables or max(threads, 64)
+    times = []
+    for it in range(args.warmup + args.steps):
+        secs, ev = ref.bench_decode_cycles(tables, C, B, cfg["d"], threads, 1, seed=it + 1)
+        assert ev == tables, (ev, tables)
+        if it >= args.warmup:
+            times.append(secs)
+    per_step = sum(times) / len(times)
+    bytes_step = tables * (k2_bytes_per_table(C, row_alg) + B * (row_alg + 4))
+    value = bytes_step / per_step / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(per_step * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) (reference GaussianStream)",
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "tables_sampled": tables,
+                   "cycle": "B=16 decode_step calls per table incl. one PagedEviction trigger"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{tables} tables x 1 eviction cycle per step "
+                                   f"(make_kv + EvictionPolicy::decode_step x16), identity-prefilled to C"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "p50_evict_step_us_per_table": round(statistics.median(times) / tables * threads * 1e6, 3),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, args):
+    """Reference CPU path on the host cores, bounded sample (~10-30 s)."""
+    try:
+        import oracle
+
+        ref = oracle.Reference()
+    except Exception as exc:  # reference library not built
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {exc}"}
+    threads = os.cpu_count() or 1
+    tables = args.ref_tables or max(threads, 64)
+    row_alg = 2 * cfg["d"] * (2 if cfg["dtype"] == "bf16" else 4)
+    secs, ev = ref.bench_decode_cycles(tables, cfg["C"], B, cfg["d"], threads, 1, seed=7)
+    bytes_step = tables * (k2_bytes_per_table(cfg["C"], row_alg) + B * (row_alg + 4))
+    return {"value": round(bytes_step / secs / 1e9, 3), "unit": "GB/s", "cores": threads,
+            "kind": "reference",
+            "sample": f"{tables} tables x 1 eviction cycle (16 decode_step incl. 1 trigger), "
+                      f"{secs:.2f} s wall"}
+
+
+# --------------------------------------------------------------------------- B200 arm
+def run_b200(args, cfg, world, rank, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_04377_b200 as pe
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peak, peak_kind = load_peaks()
+    bf16 = cfg["dtype"] == "bf16"
+    tdt = torch.bfloat16 if bf16 else torch.float32
+    elt = 2 if bf16 else 4
+    S, NL, H, d, L, C, QH = (cfg["seqs"], cfg["layers"], cfg["kvh"], cfg["d"], cfg["L"], cfg["C"],
+                             cfg["qh"])
+    G = QH // H
+    row = 2 * d * elt  # K+V
+    geo = pe.EngineGeometry(n_seqs=S, n_layers=NL, n_kv_heads=H, head_dim=d,
+                            dtype=pe.DTYPE_BF16 if bf16 else pe.DTYPE_F32, device=local)
+    eng = pe.PagedEvictionEngine(geo, pe.PolicyConfig(cache_budget=C, page_size=B))
+    stream = torch.cuda.current_stream()
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(20250904 + 3 + 1000 * rank)
+
+    # ---------------- setup: K1 prefill prune+pack of every layer (event-timed)
+    cu = np.arange(S + 1, dtype=np.int32) * L
+    k_in = torch.empty((S * L, H, d), dtype=tdt, device=dev)
+    v_in = torch.empty_like(k_in)
+    pre_ms = []
+    for layer in range(NL):
+        k_in.normal_(generator=gen)
+        v_in.normal_(generator=gen)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.prefill_compress(layer, k_in, v_in, cu)
+        e1.record(stream)
+        e1.synchronize()
+        pre_ms.append(e0.elapsed_time(e1))
+    eng.sync()
+    del k_in, v_in
+    torch.cuda.empty_cache()
+    n_tab_layer = S * H
+    k1_bytes = n_tab_layer * k1_bytes_per_table(L, C, row)
+    pre_sorted = sorted(pre_ms[1:] or pre_ms)
+    prefill = {"kernel": "K1 prefill_prune_pack (cluster of 8 CTAs per table)",
+               "ms_per_layer_p50": round(statistics.median(pre_sorted), 4),
+               "gbs": round(k1_bytes / (statistics.median(pre_sorted) * 1e-3) / 1e9, 1),
+               "tables_per_layer": n_tab_layer,
+               "algorithmic_bytes_per_layer": k1_bytes}
+    prefill["frac"] = round(prefill["gbs"] / peak, 4)
+
+    # ---------------- decode inputs: B tokens of rows for every table (device + pinned host)
+    pos = torch.full((S,), L, dtype=torch.int64, device=dev)
+    rows_k = torch.randn((B, NL, S, H, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
+    rows_v = torch.randn((B, NL, S, H, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
+    h_k = rows_k.cpu().pin_memory()
+    h_v = rows_v.cpu().pin_memory()
+    n_tab = S * NL * H
+    k2_alg = n_tab * k2_bytes_per_table(C, row)          # per step (all layers)
+    k0_alg = n_tab * B * (2 * row + 4)                   # read + write rows, positions
+    step_bytes = k2_alg + k0_alg
+    k2_per_launch = n_tab_layer * k2_bytes_per_table(C, row)
+
+    def cycle(record=None, host=False, mode=pe.ScoreMode.RECOMPUTE, victims_host=None):
+        for j in range(B):
+            if host:
+                eng.append_token(0, NL, h_k[j], h_v[j], pos)
+            else:
+                eng.append_token(0, NL, rows_k[j], rows_v[j], pos)
+            pos.add_(1)
+        for layer in range(NL):
+            if record is not None:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                eng.evict(layer, 1, step=0, mode=mode, victims=victims_host)
+                b.record(stream)
+                record.append((a, b))
+            else:
+                eng.evict(layer, 1, step=0, mode=mode, victims=victims_host)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world > 1:
+            t = torch.tensor([x], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return x
+
+    for _ in range(args.warmup):
+        cycle()
+    eng.sync()
+
+    launches0 = eng.stats().kernel_launches
+    evs = []
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            cycle(record=evs)
+        t1.record(stream)
+        barrier()
+    eng.sync()
+    launches = eng.stats().kernel_launches - launches0
+    ms_total = max_over_ranks(t0.elapsed_time(t1))
+    ms_step = ms_total / args.steps
+    k2_ms = [a.elapsed_time(b) for a, b in evs]
+    k2_mean = statistics.mean(k2_ms)
+    value = world * step_bytes / (ms_step * 1e-3) / 1e9
+    k2_gbs = k2_per_launch / (k2_mean * 1e-3) / 1e9
+
+    # ---------------- cached-score variant (K2c): p50 of the evict launch
+    evc = []
+    for _ in range(2):
+        cycle(record=evc, mode=pe.ScoreMode.CACHED)
+    eng.sync()
+    k2c_us = statistics.median([a.elapsed_time(b) * 1e3 for a, b in evc])
+
+    # ---------------- e2e: host buffers through the C-ABI
+    vict_host = np.zeros(n_tab_layer, dtype=np.int32)
+    barrier()
+    w0 = time.perf_counter()
+    for _ in range(max(1, args.steps // 2)):
+        cycle(host=True, victims_host=vict_host)
+    eng.sync()
+    barrier()
+    e2e_s = max_over_ranks((time.perf_counter() - w0) / max(1, args.steps // 2))
+    e2e = {"value": round(world * step_bytes / e2e_s / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": int(B * 2 * NL * S * H * d * elt + B * S * 8),
+           "d2h_bytes_per_step": int(NL * n_tab_layer * 4),
+           "ms_per_step": round(e2e_s * 1e3, 3)}
+
+    # ---------------- pruned decode tokens/s (K0 + K2 + K3, all layers)
+    decode = None
+    if not args.no_decode:
+        q = torch.randn((S, QH, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
+        out = torch.empty((S, QH, d), dtype=torch.float32, device=dev)
+        attn_ms = []
+        torch.cuda.synchronize()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        for j in range(B):
+            eng.append_token(0, NL, rows_k[j], rows_v[j], pos)
+            pos.add_(1)
+            for layer in range(NL):
+                if j == B - 1:
+                    eng.evict(layer, 1)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                eng.attend(layer, q, out, QH)
+                b.record(stream)
+                attn_ms.append((a, b))
+        d1.record(stream)
+        d1.synchronize()
+        dec_ms = d0.elapsed_time(d1)
+        at = [a.elapsed_time(b) for a, b in attn_ms]
+        k3_bytes = n_tab_layer * k3_bytes_per_table(C + B // 2, row, G, d, elt)
+        decode = {"tokens_per_s": round(world * S * B / (dec_ms * 1e-3), 1),
+                  "ms_per_token_all_layers": round(dec_ms / B, 4),
+                  "attention_us_per_layer_p50": round(statistics.median(at) * 1e3, 2),
+                  "attention_gbs": round(k3_bytes / (statistics.median(at) * 1e-3) / 1e9, 1)}
+
+    cpu = cpu_baseline(cfg, args) if (rank == 0 and world == 1 and not args.no_cpu) else None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
+            "data": "synthetic N(0,1) K/V/Q (torch.randn); inputs resident in HBM",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "tables_per_gpu": n_tab,
+                       "page_size": B, "step": "one eviction cycle: 16 decode appends (K0) + "
+                       "block eviction of every table (K2, per-layer launches)",
+                       "l2": "inputs larger than L2 (pool %.1f GB per GPU)" % (eng.info().pool_bytes / 1e9)},
+            "pct_of_peak": round(100 * value / world / peak, 2),
+            "p50_evict_step_us": round(statistics.median(k2_ms) * 1e3, 2),
+            "p50_evict_step_us_cached": round(k2c_us, 2),
+            "roofline": {"bound": "hbm", "achieved": round(k2_gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(k2_gbs / peak, 4), "traffic": None,
+                         "kernel": "K2 evict (plan + evict_score_kernel), per-layer launch",
+                         "algorithmic_bytes_per_launch": k2_per_launch, "peak_kind": peak_kind},
+            "prefill": prefill,
+            "decode": decode,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--ref-tables", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+    else:
+        run_b200(args, cfg, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

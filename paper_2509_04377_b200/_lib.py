@@ -1,0 +1,83 @@
+"""ctypes binding of include/pe/pe.h (libpe_b200.so).
+
+Loading fails loudly: there is no CPU fallback for the PagedEviction hot path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+from . import _build
+
+_lock = threading.Lock()
+_lib: C.CDLL | None = None
+
+c_i32, c_i64, c_vp = C.c_int32, C.c_int64, C.c_void_p
+
+
+class PeConfig(C.Structure):
+    _fields_ = [(n, c_i32) for n in (
+        "n_seqs", "n_layers", "n_kv_heads", "head_dim", "granularity", "page_size", "cache_budget",
+        "dtype", "policy", "capacity", "max_pages_per_table", "device")]
+
+
+class PeInfo(C.Structure):
+    _fields_ = [(n, c_i32) for n in (
+        "n_tables", "tab_heads", "width", "page_size", "cache_budget", "capacity", "max_pages",
+        "dtype", "policy", "granularity", "row_pitch_bytes", "sm_count")] + [
+        ("pool_bytes", c_i64), ("state_bytes", c_i64), ("free_pages", c_i32), ("pad_", c_i32)]
+
+
+class PeStats(C.Structure):
+    _fields_ = [(n, c_i64) for n in (
+        "prefill_calls", "append_calls", "evict_calls", "attention_calls", "tokens_scored",
+        "pages_evicted", "kernel_launches")]
+
+
+class PeDeviceView(C.Structure):
+    _fields_ = [("pages", c_vp), ("block_table", c_vp), ("num_pages", c_vp),
+                ("newest_fill", c_vp), ("retained", c_vp), ("positions", c_vp)]
+
+
+# every symbol include/pe/pe.h declares, with its signature
+SIGNATURES = {
+    "pe_abi_version": (c_i32, []),
+    "pe_last_error": (C.c_char_p, []),
+    "pe_status_string": (C.c_char_p, [C.c_int]),
+    "pe_engine_create": (C.c_int, [C.POINTER(PeConfig), C.POINTER(c_vp)]),
+    "pe_engine_destroy": (C.c_int, [c_vp]),
+    "pe_prefill_prune_pack": (C.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "pe_decode_append": (C.c_int, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "pe_decode_evict": (C.c_int, [c_vp, c_i32, c_i32, c_i64, c_i32, c_vp, c_vp]),
+    "pe_decode_step": (C.c_int, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "pe_paged_decode_attention": (C.c_int, [c_vp, c_i32, c_vp, c_vp, c_i32, c_vp]),
+    "pe_sync": (C.c_int, [c_vp]),
+    "pe_get_info": (C.c_int, [c_vp, C.POINTER(PeInfo)]),
+    "pe_get_stats": (C.c_int, [c_vp, C.POINTER(PeStats)]),
+    "pe_read_tables": (C.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pe_read_free_list": (C.c_int, [c_vp, c_vp, C.POINTER(c_i32)]),
+    "pe_read_positions": (C.c_int, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
+    "pe_read_pages": (C.c_int, [c_vp, c_i32, c_i32, c_vp]),
+    "pe_get_device_view": (C.c_int, [c_vp, C.POINTER(PeDeviceView)]),
+}
+
+
+def load() -> C.CDLL:
+    """Builds (if stale) and loads libpe_b200.so. Raises if it cannot."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            path = _build.build()
+            lib = C.CDLL(str(path))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            if lib.pe_abi_version() != 1:
+                raise RuntimeError("libpe_b200.so ABI version mismatch")
+            _lib = lib
+    return _lib
+
+
+def library_path() -> str:
+    return str(_build.LIB)

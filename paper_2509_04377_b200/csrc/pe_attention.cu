@@ -1,0 +1,271 @@
+// K3: GQA paged decode attention over the pruned block tables.
+//
+// Reference: attend (attention.cpp:15-99) — per query head, logits
+// q.k/sqrt(d) over the retained tokens in logical order (for_each_retained,
+// block_table.hpp:81-91), max-subtracted softmax, weighted sum of values.
+// The reference is MHA in double; GQA is the reference's attend called once
+// per query head (head_count = 1) on its KV head's table (D3).
+// Tolerance: relative L2 (output_deviation, attention.cpp:105-118) 1e-5 for
+// fp32 caches, 1e-3 for bf16.
+//
+// Split-K: CTA (split, table) owns a contiguous range of the table's pages;
+// each warp streams whole pages (K slots then V slots, 2B contiguous rows)
+// into padded shared memory with cp.async, computes the G heads' logits with
+// one lane per (token, head-pair), runs an online softmax in fp32 (exp2 with
+// log2e folded into the scale) and accumulates P.V with one lane per
+// d/32-dimension slice. Warp and split partials are merged with the usual
+// (max, sum) log-sum-exp rescaling.
+#include "pe_kernels.cuh"
+
+namespace pe {
+
+constexpr int kAttnThreads = 128;
+constexpr int kAttnMaxG = 8;
+constexpr int kAttnMaxDpl = 8;  // d <= 256
+constexpr int kAttnStages = 2;
+
+__device__ __forceinline__ float elem_f32(const uint8_t* row, int idx, int dtype) {
+    if (dtype == PE_DTYPE_BF16) {
+        return __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(row)[idx]) << 16);
+    }
+    return reinterpret_cast<const float*>(row)[idx];
+}
+
+__global__ void __launch_bounds__(kAttnThreads) attention_split_kernel(DevState s, AttnArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    const int i = blockIdx.y;            // launch table: seq * H + h
+    const int sp = blockIdx.x;           // split
+    const int H = s.tab_heads;
+    const int h = i % H;
+    const int seq = i / H;
+    const int t = (seq * s.n_layers + a.layer) * H + h;
+    const int G = a.G;
+    const int d = s.w;
+    const int B = s.B;
+    const int N = s.num_pages[t];
+    const int p_begin = sp * a.pages_per_split;
+    const int p_end = min(N, p_begin + a.pages_per_split);
+    const int row_pitch = s.row_bytes + 16;
+    const int stage_bytes = 2 * B * row_pitch;
+
+    // shared layout: q [G][d] float | p [nw][G][16] float | warp partials | stages
+    float* q_sm = reinterpret_cast<float*>(smem);
+    float* p_sm = q_sm + G * d;
+    float* wpart_o = p_sm + nw * G * 16;          // [nw][G][d]
+    float* wpart_ml = wpart_o + nw * G * d;       // [nw][G][2]
+    uint8_t* stages = reinterpret_cast<uint8_t*>(wpart_ml + nw * G * 2);
+    stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(stages) + 15) & ~uintptr_t(15));
+    uint8_t* my_stage = stages + wid * kAttnStages * stage_bytes;
+
+    // load the G query heads of this table (as float, pre-scaled by log2e/sqrt(d))
+    for (int x = threadIdx.x; x < G * d; x += blockDim.x) {
+        const int g = x / d;
+        const int dd = x % d;
+        const uint8_t* qrow = a.q + ((int64_t)seq * a.n_q_heads + h * G + g) * s.row_bytes;
+        q_sm[x] = elem_f32(qrow, dd, s.dtype) * a.scale_log2;
+    }
+    __syncthreads();
+
+    const int dpl = (d + 31) / 32;  // dims per lane in P.V
+    float o[kAttnMaxG][kAttnMaxDpl];
+    float m[kAttnMaxG], l[kAttnMaxG];
+#pragma unroll
+    for (int g = 0; g < kAttnMaxG; ++g) {
+        m[g] = -INFINITY;
+        l[g] = 0.f;
+#pragma unroll
+        for (int k = 0; k < kAttnMaxDpl; ++k) o[g][k] = 0.f;
+    }
+
+    const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
+    const int my_n = (p_end - p_begin) > wid ? ((p_end - p_begin) - wid + nw - 1) / nw : 0;
+    const int pieces = s.row_bytes / 16;
+    auto issue = [&](int k) {
+        if (k < my_n) {
+            const int pg = p_begin + wid + k * nw;
+            const uint8_t* base = s.pages + (int64_t)row[pg] * 2 * B * s.pitch;
+            const int fill = (pg == N - 1) ? s.newest_fill[t] : B;
+            uint8_t* st = my_stage + (k % kAttnStages) * stage_bytes;
+            const int total = 2 * B * pieces;
+            for (int x = lane; x < total; x += 32) {
+                const int r = x / pieces;
+                const int pc = x - r * pieces;
+                const int slot = r % B;
+                if (slot < fill) cp_async16(st + r * row_pitch + pc * 16, base + (int64_t)r * s.pitch + pc * 16);
+            }
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < kAttnStages - 1; ++k) issue(k);
+
+    float* my_p = p_sm + wid * G * 16;
+    for (int k = 0; k < my_n; ++k) {
+        issue(k + kAttnStages - 1);
+        cp_async_wait<kAttnStages - 1>();
+        __syncwarp();
+        const int pg = p_begin + wid + k * nw;
+        const int fill = (pg == N - 1) ? s.newest_fill[t] : B;
+        const uint8_t* st = my_stage + (k % kAttnStages) * stage_bytes;
+        // process the page in groups of 16 slots
+        for (int s0 = 0; s0 < fill; s0 += 16) {
+            const int ns = min(16, fill - s0);
+            // logits: lane -> slot s0 + (lane & 15), heads g = (lane>>4), +2, ...
+            const int slot = s0 + (lane & 15);
+            float sc[kAttnMaxG / 2];
+#pragma unroll
+            for (int gg = 0; gg < kAttnMaxG / 2; ++gg) sc[gg] = -INFINITY;
+            if ((lane & 15) < ns) {
+                const uint8_t* krow = st + slot * row_pitch;
+                float acc[kAttnMaxG / 2];
+#pragma unroll
+                for (int gg = 0; gg < kAttnMaxG / 2; ++gg) acc[gg] = 0.f;
+                for (int dd = 0; dd < d; dd += 4) {
+                    float kv[4];
+                    if (s.dtype == PE_DTYPE_BF16) {
+                        const uint2 u = *reinterpret_cast<const uint2*>(krow + dd * 2);
+                        kv[0] = __uint_as_float(u.x << 16);
+                        kv[1] = __uint_as_float(u.x & 0xFFFF0000u);
+                        kv[2] = __uint_as_float(u.y << 16);
+                        kv[3] = __uint_as_float(u.y & 0xFFFF0000u);
+                    } else {
+                        const float4 f = *reinterpret_cast<const float4*>(krow + dd * 4);
+                        kv[0] = f.x; kv[1] = f.y; kv[2] = f.z; kv[3] = f.w;
+                    }
+#pragma unroll
+                    for (int gg = 0; gg < kAttnMaxG / 2; ++gg) {
+                        const int g = (lane >> 4) + 2 * gg;
+                        if (g < G) {
+                            const float4 qv = *reinterpret_cast<const float4*>(q_sm + g * d + dd);
+                            acc[gg] = fmaf(qv.x, kv[0], acc[gg]);
+                            acc[gg] = fmaf(qv.y, kv[1], acc[gg]);
+                            acc[gg] = fmaf(qv.z, kv[2], acc[gg]);
+                            acc[gg] = fmaf(qv.w, kv[3], acc[gg]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int gg = 0; gg < kAttnMaxG / 2; ++gg) sc[gg] = acc[gg];
+            }
+            // online softmax per head over the 16 slots (lanes of the same half)
+#pragma unroll
+            for (int gg = 0; gg < kAttnMaxG / 2; ++gg) {
+                float mx = sc[gg];
+#pragma unroll
+                for (int off = 8; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
+                const int g = (lane >> 4) + 2 * gg;
+                // both halves hold different heads; broadcast via smem
+                const float mg_old = (g < G) ? m[g] : -INFINITY;
+                const float mnew = fmaxf(mg_old, mx);
+                const float pexp = (g < G && (lane & 15) < ns) ? exp2f(sc[gg] - mnew) : 0.f;
+                float ps = pexp;
+#pragma unroll
+                for (int off = 8; off > 0; off >>= 1) ps += __shfl_xor_sync(0xFFFFFFFFu, ps, off);
+                if (g < G) my_p[g * 16 + (lane & 15)] = pexp;
+                const float mnew_b = mnew;
+                const float ps_b = ps;
+                // lanes 0 and 16 hold heads 2gg and 2gg+1: broadcast to every lane
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const int gh = half + 2 * gg;
+                    const float mn = __shfl_sync(0xFFFFFFFFu, mnew_b, half * 16);
+                    const float pss = __shfl_sync(0xFFFFFFFFu, ps_b, half * 16);
+                    if (gh < G) {
+                        const float corr = exp2f(m[gh] - mn);
+                        l[gh] = l[gh] * corr + pss;
+#pragma unroll
+                        for (int kk = 0; kk < kAttnMaxDpl; ++kk) o[gh][kk] *= corr;
+                        m[gh] = mn;
+                    }
+                }
+            }
+            __syncwarp();
+            // P.V: lane owns dims lane + 32*k
+            for (int j = 0; j < ns; ++j) {
+                const uint8_t* vrow = st + (B + s0 + j) * row_pitch;
+                float vv[kAttnMaxDpl];
+#pragma unroll
+                for (int kk = 0; kk < kAttnMaxDpl; ++kk) {
+                    const int dd = lane + 32 * kk;
+                    vv[kk] = (kk < dpl && dd < d) ? elem_f32(vrow, dd, s.dtype) : 0.f;
+                }
+#pragma unroll
+                for (int g = 0; g < kAttnMaxG; ++g) {
+                    if (g < G) {
+                        const float p = my_p[g * 16 + j];
+#pragma unroll
+                        for (int kk = 0; kk < kAttnMaxDpl; ++kk) o[g][kk] = fmaf(p, vv[kk], o[g][kk]);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+    }
+    cp_async_wait<0>();
+
+    // warp partials -> smem
+    float* wo = wpart_o + wid * G * d;
+    float* wml = wpart_ml + wid * G * 2;
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int kk = 0; kk < kAttnMaxDpl; ++kk) {
+            const int dd = lane + 32 * kk;
+            if (kk < dpl && dd < d) wo[g * d + dd] = o[g][kk];
+        }
+        if (lane == 0) {
+            wml[g * 2] = m[g];
+            wml[g * 2 + 1] = l[g];
+        }
+    }
+    __syncthreads();
+    // merge the warps and write the split partial
+    const int n_splits = a.splits;
+    for (int x = threadIdx.x; x < G * d; x += blockDim.x) {
+        const int g = x / d;
+        float mm = -INFINITY;
+        for (int w2 = 0; w2 < nw; ++w2) mm = fmaxf(mm, wpart_ml[w2 * G * 2 + g * 2]);
+        float ll = 0.f, oo = 0.f;
+        for (int w2 = 0; w2 < nw; ++w2) {
+            const float mw = wpart_ml[w2 * G * 2 + g * 2];
+            const float c = (mw == -INFINITY) ? 0.f : exp2f(mw - mm);
+            ll += wpart_ml[w2 * G * 2 + g * 2 + 1] * c;
+            oo += wpart_o[w2 * G * d + x] * c;
+        }
+        const int64_t pidx = ((int64_t)i * n_splits + sp) * G + g;
+        a.part_o[pidx * d + (x % d)] = oo;
+        if (x % d == 0) {
+            a.part_ml[pidx * 2] = mm;
+            a.part_ml[pidx * 2 + 1] = ll;
+        }
+    }
+}
+
+// merge the split partials: out = sum_s o_s * 2^(m_s - M) / sum_s l_s * 2^(m_s - M)
+__global__ void __launch_bounds__(128) attention_merge_kernel(DevState s, AttnArgs a) {
+    const int i = blockIdx.x;  // launch table
+    const int H = s.tab_heads;
+    const int h = i % H;
+    const int seq = i / H;
+    const int G = a.G;
+    const int d = s.w;
+    for (int x = threadIdx.x; x < G * d; x += blockDim.x) {
+        const int g = x / d;
+        float mm = -INFINITY;
+        for (int sp = 0; sp < a.splits; ++sp) mm = fmaxf(mm, a.part_ml[(((int64_t)i * a.splits + sp) * G + g) * 2]);
+        float ll = 0.f, oo = 0.f;
+        for (int sp = 0; sp < a.splits; ++sp) {
+            const int64_t pidx = ((int64_t)i * a.splits + sp) * G + g;
+            const float ms = a.part_ml[pidx * 2];
+            const float c = (ms == -INFINITY) ? 0.f : exp2f(ms - mm);
+            ll += a.part_ml[pidx * 2 + 1] * c;
+            oo += a.part_o[pidx * d + (x % d)] * c;
+        }
+        a.out[((int64_t)seq * a.n_q_heads + h * G + g) * d + (x % d)] = oo / ll;
+    }
+}
+
+}  // namespace pe

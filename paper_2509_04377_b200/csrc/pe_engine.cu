@@ -1,0 +1,650 @@
+// Host side of the C-ABI (include/pe/pe.h): engine lifecycle, argument
+// validation (mirroring the reference's exceptions as pe_status codes),
+// host-buffer staging, and the launch sequences of K0/K1/K2/K3.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pe_kernels.cuh"
+
+using namespace pe;
+
+namespace {
+
+thread_local std::string g_err;
+
+pe_status fail(pe_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+#define PE_CUDA(call)                                                                  \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess) {                                                       \
+            return fail(PE_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+        }                                                                              \
+    } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t n) {
+    return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T));
+}
+
+bool is_device_ptr(const void* p) {
+    if (p == nullptr) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct pe_engine {
+    pe_config cfg{};
+    DevState s{};
+    int device = 0;
+    int sm_count = 0;
+    int32_t tab_heads = 0;
+    // scratch
+    LaunchCtl* ctl = nullptr;
+    int32_t* rank = nullptr;
+    int32_t* work = nullptr;
+    int32_t* victims = nullptr;
+    int32_t* tickets = nullptr;
+    double* evict_scratch = nullptr;
+    int32_t* tab_len = nullptr;
+    int64_t* tab_tok0 = nullptr;
+    int32_t* tab_pagebase = nullptr;
+    int32_t* evicted_dev = nullptr;
+    int32_t* h_tab_len = nullptr;       // pinned
+    int64_t* h_tab_tok0 = nullptr;      // pinned
+    int32_t* h_tab_pagebase = nullptr;  // pinned
+    // staging for host buffers
+    uint8_t* stage_a = nullptr;
+    size_t stage_a_bytes = 0;
+    uint8_t* stage_b = nullptr;
+    size_t stage_b_bytes = 0;
+    uint8_t* stage_c = nullptr;
+    size_t stage_c_bytes = 0;
+    float* part_o = nullptr;
+    size_t part_o_elems = 0;
+    float* part_ml = nullptr;
+    size_t part_ml_elems = 0;
+    float* out_stage = nullptr;
+    size_t out_stage_elems = 0;
+    pe_stats stats{};
+};
+
+namespace {
+
+pe_status ensure(uint8_t** buf, size_t* have, size_t need) {
+    if (*have >= need) return PE_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *have = 0;
+    PE_CUDA(cudaMalloc(buf, need));
+    *have = need;
+    return PE_OK;
+}
+
+template <typename T>
+pe_status ensure_t(T** buf, size_t* have, size_t need) {
+    if (*have >= need) return PE_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *have = 0;
+    PE_CUDA(dalloc(buf, need));
+    *have = need;
+    return PE_OK;
+}
+
+// Device view of an input buffer: device pointers pass through; host
+// buffers are copied into engine staging on `st`.
+pe_status as_device(pe_engine* e, const void* p, size_t bytes, uint8_t** stage, size_t* have,
+                    cudaStream_t st, const uint8_t** out) {
+    if (p == nullptr) return fail(PE_INVALID_ARG, "null buffer");
+    if (is_device_ptr(p)) {
+        *out = static_cast<const uint8_t*>(p);
+        return PE_OK;
+    }
+    pe_status r = ensure(stage, have, bytes);
+    if (r != PE_OK) return r;
+    PE_CUDA(cudaMemcpyAsync(*stage, p, bytes, cudaMemcpyHostToDevice, st));
+    *out = *stage;
+    (void)e;
+    return PE_OK;
+}
+
+int32_t elt_size(int32_t dtype) { return dtype == PE_DTYPE_BF16 ? 2 : 4; }
+
+pe_status check_launch(pe_engine* e, const char* what) {
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return fail(PE_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(err));
+    (void)e;
+    return PE_OK;
+}
+
+constexpr int kEvictPagesPerCta = 32;
+
+}  // namespace
+
+extern "C" {
+
+int32_t pe_abi_version(void) { return PE_ABI_VERSION; }
+
+const char* pe_last_error(void) { return g_err.c_str(); }
+
+const char* pe_status_string(pe_status s) {
+    switch (s) {
+    case PE_OK: return "ok";
+    case PE_ERROR: return "error";
+    case PE_POOL_EXHAUSTED: return "page pool exhausted";
+    case PE_INDEX_OUT_OF_RANGE: return "index out of range";
+    case PE_UNKNOWN_POSITION: return "unknown position";
+    case PE_OVERFLOW: return "overflow";
+    case PE_EMPTY_PAGE: return "page has no occupied slots";
+    case PE_K_TOO_LARGE: return "k too large";
+    case PE_NO_ELIGIBLE_PAGE: return "no eligible page to rank";
+    case PE_BUDGET_INVALID: return "budget invalid";
+    case PE_EMPTY_CACHE: return "attention requires at least one retained token";
+    case PE_LENGTH_MISMATCH: return "length mismatch";
+    case PE_EMPTY_INPUT: return "empty input";
+    case PE_IO_ERROR: return "io error";
+    case PE_INVALID_ARG: return "invalid argument";
+    case PE_INVALID_STATE: return "invalid state";
+    case PE_CUDA_ERROR: return "cuda error";
+    case PE_NO_DEVICE: return "no usable sm_100 device";
+    }
+    return "unknown status";
+}
+
+pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
+    if (cfg_in == nullptr || out == nullptr) return fail(PE_INVALID_ARG, "null argument");
+    *out = nullptr;
+    pe_config c = *cfg_in;
+    // PolicyConfig::validate (policy.cpp:38-52)
+    if (c.page_size <= 0) return fail(PE_BUDGET_INVALID, "page size must be positive");
+    if (c.cache_budget < c.page_size)
+        return fail(PE_BUDGET_INVALID, "budget must be at least one page (" + std::to_string(c.page_size) + " tokens)");
+    if (c.cache_budget % c.page_size != 0) return fail(PE_BUDGET_INVALID, "budget must be a multiple of page size");
+    if (c.policy != PE_POLICY_PAGED_EVICTION && c.policy != PE_POLICY_FULL_CACHE)
+        return fail(PE_INVALID_ARG, "policy must be PagedEviction or FullCache");
+    if (c.dtype != PE_DTYPE_F32 && c.dtype != PE_DTYPE_BF16) return fail(PE_INVALID_ARG, "dtype");
+    if (c.granularity != PE_GRANULARITY_PER_KV_HEAD && c.granularity != PE_GRANULARITY_PER_LAYER)
+        return fail(PE_INVALID_ARG, "granularity");
+    if (c.n_seqs <= 0 || c.n_layers <= 0 || c.n_kv_heads <= 0 || c.head_dim <= 0)
+        return fail(PE_INVALID_ARG, "geometry must be positive");
+    const int32_t tab_heads = c.granularity == PE_GRANULARITY_PER_KV_HEAD ? c.n_kv_heads : 1;
+    const int32_t w = c.granularity == PE_GRANULARITY_PER_KV_HEAD ? c.head_dim : c.n_kv_heads * c.head_dim;
+    const int32_t row_bytes = w * elt_size(c.dtype);
+    if (row_bytes % 16 != 0)
+        return fail(PE_INVALID_ARG, "row width * element size must be a multiple of 16 bytes");
+    const int64_t n_tables64 = (int64_t)c.n_seqs * c.n_layers * tab_heads;
+    if (n_tables64 > (1 << 30)) return fail(PE_OVERFLOW, "too many tables");
+    const int32_t n_tables = static_cast<int32_t>(n_tables64);
+    int32_t max_pages = c.max_pages_per_table;
+    if (max_pages <= 0) {
+        if (c.policy == PE_POLICY_FULL_CACHE)
+            return fail(PE_INVALID_ARG, "FullCache needs max_pages_per_table");
+        max_pages = c.cache_budget / c.page_size + 1;
+    }
+    int64_t cap = c.capacity > 0 ? c.capacity : (int64_t)n_tables * max_pages;
+    if (cap >= (int64_t)1 << 31) return fail(PE_OVERFLOW, "pool capacity exceeds int32 page ids");
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(PE_NO_DEVICE, "no CUDA device");
+    }
+    if (c.device < 0 || c.device >= ndev) return fail(PE_NO_DEVICE, "device ordinal out of range");
+    cudaDeviceProp prop{};
+    PE_CUDA(cudaGetDeviceProperties(&prop, c.device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(PE_NO_DEVICE, "engine is built for sm_100a (B200); device is sm_" +
+                                      std::to_string(prop.major) + std::to_string(prop.minor));
+    PE_CUDA(cudaSetDevice(c.device));
+
+    auto* e = new pe_engine();
+    e->cfg = c;
+    e->device = c.device;
+    e->sm_count = prop.multiProcessorCount;
+    e->tab_heads = tab_heads;
+    DevState& s = e->s;
+    s.capacity = static_cast<int32_t>(cap);
+    s.B = c.page_size;
+    s.C = c.cache_budget;
+    s.w = w;
+    s.row_bytes = row_bytes;
+    s.pitch = row_bytes;
+    s.max_pages = max_pages;
+    s.n_tables = n_tables;
+    s.n_seqs = c.n_seqs;
+    s.n_layers = c.n_layers;
+    s.tab_heads = tab_heads;
+    s.dtype = c.dtype;
+    s.policy = c.policy;
+
+    auto cleanup_fail = [&](pe_status st) {
+        pe_engine_destroy(e);
+        return st;
+    };
+    const size_t page_bytes = (size_t)2 * s.B * s.pitch;
+    if (cudaMalloc(&s.pages, (size_t)cap * page_bytes) != cudaSuccess ||
+        dalloc(&s.positions, (size_t)cap * s.B) != cudaSuccess ||
+        dalloc(&s.token_scores, (size_t)cap * s.B) != cudaSuccess ||
+        dalloc(&s.page_scores, (size_t)cap) != cudaSuccess ||
+        dalloc(&s.block_table, (size_t)n_tables * max_pages) != cudaSuccess ||
+        dalloc(&s.num_pages, n_tables) != cudaSuccess || dalloc(&s.newest_fill, n_tables) != cudaSuccess ||
+        dalloc(&s.retained, n_tables) != cudaSuccess || dalloc(&s.stack, (size_t)cap) != cudaSuccess ||
+        dalloc(&s.top, 1) != cudaSuccess || dalloc(&s.status, 1) != cudaSuccess ||
+        dalloc(&s.evict_count, 1) != cudaSuccess || dalloc(&e->ctl, 1) != cudaSuccess ||
+        dalloc(&e->rank, n_tables) != cudaSuccess || dalloc(&e->work, n_tables) != cudaSuccess ||
+        dalloc(&e->victims, n_tables) != cudaSuccess || dalloc(&e->tickets, n_tables) != cudaSuccess ||
+        dalloc(&e->evict_scratch, (size_t)n_tables * max_pages) != cudaSuccess ||
+        dalloc(&e->tab_len, (size_t)c.n_seqs * tab_heads) != cudaSuccess ||
+        dalloc(&e->tab_tok0, (size_t)c.n_seqs * tab_heads) != cudaSuccess ||
+        dalloc(&e->tab_pagebase, (size_t)c.n_seqs * tab_heads) != cudaSuccess ||
+        dalloc(&e->evicted_dev, (size_t)c.n_seqs * tab_heads) != cudaSuccess) {
+        cudaGetLastError();
+        return cleanup_fail(fail(PE_CUDA_ERROR, "device allocation failed (pool of " +
+                                                    std::to_string(cap) + " pages)"));
+    }
+    if (cudaMallocHost(&e->h_tab_len, sizeof(int32_t) * c.n_seqs * tab_heads) != cudaSuccess ||
+        cudaMallocHost(&e->h_tab_tok0, sizeof(int64_t) * c.n_seqs * tab_heads) != cudaSuccess ||
+        cudaMallocHost(&e->h_tab_pagebase, sizeof(int32_t) * c.n_seqs * tab_heads) != cudaSuccess) {
+        cudaGetLastError();
+        return cleanup_fail(fail(PE_CUDA_ERROR, "pinned allocation failed"));
+    }
+    // LIFO free list initialised [cap-1, ..., 0] (page_pool.cpp:18-21)
+    {
+        std::vector<int32_t> stack(cap);
+        for (int64_t i = 0; i < cap; ++i) stack[i] = static_cast<int32_t>(cap - 1 - i);
+        const int32_t top = static_cast<int32_t>(cap);
+        if (cudaMemcpy(s.stack, stack.data(), sizeof(int32_t) * cap, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s.top, &top, sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemset(s.block_table, 0xFF, sizeof(int32_t) * (size_t)n_tables * max_pages) != cudaSuccess ||
+            cudaMemset(s.num_pages, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
+            cudaMemset(s.newest_fill, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
+            cudaMemset(s.retained, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
+            cudaMemset(s.status, 0, sizeof(int32_t)) != cudaSuccess ||
+            cudaMemset(s.evict_count, 0, sizeof(unsigned long long)) != cudaSuccess ||
+            cudaMemset(e->tickets, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
+            cudaMemset(s.positions, 0xFF, sizeof(int32_t) * (size_t)cap * s.B) != cudaSuccess ||
+            cudaMemset(s.pages, 0, (size_t)cap * page_bytes) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess) {
+            cudaGetLastError();
+            return cleanup_fail(fail(PE_CUDA_ERROR, "state initialisation failed"));
+        }
+    }
+    // kernel attributes (dynamic smem beyond 48 KB)
+    cudaFuncSetAttribute(evict_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (kEvictThreads / 32) * kEvictStages * kStageBytes);
+    cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(attention_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaGetLastError();
+    *out = e;
+    return PE_OK;
+}
+
+pe_status pe_engine_destroy(pe_engine* e) {
+    if (e == nullptr) return PE_OK;
+    cudaSetDevice(e->device);
+    cudaDeviceSynchronize();
+    DevState& s = e->s;
+    void* dev[] = {s.pages, s.positions, s.token_scores, s.page_scores, s.block_table, s.num_pages,
+                   s.newest_fill, s.retained, s.stack, s.top, s.status, s.evict_count, e->ctl, e->rank,
+                   e->work, e->victims, e->tickets, e->evict_scratch, e->tab_len, e->tab_tok0,
+                   e->tab_pagebase, e->evicted_dev, e->stage_a, e->stage_b, e->stage_c, e->part_o,
+                   e->part_ml, e->out_stage};
+    for (void* p : dev) {
+        if (p) cudaFree(p);
+    }
+    if (e->h_tab_len) cudaFreeHost(e->h_tab_len);
+    if (e->h_tab_tok0) cudaFreeHost(e->h_tab_tok0);
+    if (e->h_tab_pagebase) cudaFreeHost(e->h_tab_pagebase);
+    cudaGetLastError();
+    delete e;
+    return PE_OK;
+}
+
+// ------------------------------------------------------------------ K1
+pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, const void* v,
+                                const int32_t* cu_seqlens, int32_t seq_begin, int32_t n_seqs,
+                                int32_t* evicted_counts, void* stream) {
+    if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
+    const DevState& s = e->s;
+    if (layer < 0 || layer >= s.n_layers) return fail(PE_INVALID_ARG, "layer out of range");
+    if (seq_begin < 0 || n_seqs <= 0 || seq_begin + n_seqs > s.n_seqs)
+        return fail(PE_INVALID_ARG, "sequence range out of range");
+    if (cu_seqlens == nullptr) return fail(PE_INVALID_ARG, "cu_seqlens");
+    if (cu_seqlens[0] != 0) return fail(PE_INVALID_ARG, "cu_seqlens[0] must be 0");
+    cudaSetDevice(e->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int H = s.tab_heads;
+    const int n_tab = n_seqs * H;
+    int64_t total_pages = 0;
+    int max_len = 0;
+    for (int q = 0; q < n_seqs; ++q) {
+        const int L = cu_seqlens[q + 1] - cu_seqlens[q];
+        if (L <= 0) return fail(PE_ERROR, "prefill requires at least one token");  // policy.cpp:57-58
+        const int keep = (s.policy == PE_POLICY_PAGED_EVICTION && L > s.C) ? s.C : L;
+        const int np = (keep + s.B - 1) / s.B;
+        if (np > s.max_pages)
+            return fail(PE_INVALID_ARG, "prefill of " + std::to_string(L) + " tokens exceeds max_pages_per_table");
+        max_len = std::max(max_len, L);
+        for (int h = 0; h < H; ++h) {
+            const int i = q * H + h;
+            e->h_tab_len[i] = L;
+            e->h_tab_tok0[i] = cu_seqlens[q];
+            e->h_tab_pagebase[i] = static_cast<int32_t>(total_pages);
+            total_pages += np;
+        }
+    }
+    const int chunk_cap = (max_len + kPrefillCluster - 1) / kPrefillCluster;
+    const int keys_bytes = ((chunk_cap * 8) + 15) & ~15;
+    const int stage_bytes = (kPrefillThreads / 32) * kPrefillStages * kStageBytes;
+    if (chunk_cap * 4 > stage_bytes || keys_bytes + stage_bytes > 227 * 1024 - 4096)
+        return fail(PE_INVALID_ARG, "prefill length " + std::to_string(max_len) +
+                                        " exceeds the per-cluster shared-memory capacity");
+    const size_t tokens = cu_seqlens[n_seqs];
+    const size_t in_bytes = tokens * (size_t)H * s.row_bytes;
+    const uint8_t *dk = nullptr, *dv = nullptr;
+    pe_status r = as_device(e, k, in_bytes, &e->stage_a, &e->stage_a_bytes, st, &dk);
+    if (r != PE_OK) return r;
+    r = as_device(e, v, in_bytes, &e->stage_b, &e->stage_b_bytes, st, &dv);
+    if (r != PE_OK) return r;
+    PE_CUDA(cudaMemcpyAsync(e->tab_len, e->h_tab_len, sizeof(int32_t) * n_tab, cudaMemcpyHostToDevice, st));
+    PE_CUDA(cudaMemcpyAsync(e->tab_tok0, e->h_tab_tok0, sizeof(int64_t) * n_tab, cudaMemcpyHostToDevice, st));
+    PE_CUDA(cudaMemcpyAsync(e->tab_pagebase, e->h_tab_pagebase, sizeof(int32_t) * n_tab, cudaMemcpyHostToDevice, st));
+    const bool ev_dev = evicted_counts && is_device_ptr(evicted_counts);
+    PrefillArgs a{};
+    a.k = dk;
+    a.v = dv;
+    a.token_stride = (int64_t)H * s.row_bytes;
+    a.tab_len = e->tab_len;
+    a.tab_tok0 = e->tab_tok0;
+    a.tab_pagebase = e->tab_pagebase;
+    a.evicted_counts = evicted_counts ? (ev_dev ? evicted_counts : e->evicted_dev) : nullptr;
+    a.n_tab = n_tab;
+    a.seq_begin = seq_begin;
+    a.layer = layer;
+    a.chunk_cap = chunk_cap;
+    if (total_pages > INT32_MAX) return fail(PE_POOL_EXHAUSTED, "page pool exhausted");
+    plan_prefill_kernel<<<1, 1024, 0, st>>>(s, a, static_cast<int32_t>(total_pages), e->ctl);
+    prefill_kernel<<<dim3(kPrefillCluster, n_tab), kPrefillThreads, keys_bytes + stage_bytes, st>>>(s, a, e->ctl);
+    r = check_launch(e, "prefill_kernel");
+    if (r != PE_OK) return r;
+    e->stats.kernel_launches += 2;
+    e->stats.prefill_calls += 1;
+    e->stats.tokens_scored += (int64_t)tokens * H;
+    if (evicted_counts && !ev_dev) {
+        PE_CUDA(cudaMemcpyAsync(evicted_counts, e->evicted_dev, sizeof(int32_t) * n_tab, cudaMemcpyDeviceToHost, st));
+    }
+    return PE_OK;
+}
+
+// ------------------------------------------------------------------ K0
+pe_status pe_decode_append(pe_engine* e, int32_t layer_begin, int32_t n_layers, const void* k_rows,
+                           const void* v_rows, const int64_t* positions, void* stream) {
+    if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
+    const DevState& s = e->s;
+    if (layer_begin < 0 || n_layers <= 0 || layer_begin + n_layers > s.n_layers)
+        return fail(PE_INVALID_ARG, "layer range out of range");
+    cudaSetDevice(e->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TableSet ts{layer_begin, n_layers};
+    const int n = ts.size(s);
+    const size_t bytes = (size_t)n * s.row_bytes;
+    const uint8_t *dk = nullptr, *dv = nullptr, *dp = nullptr;
+    pe_status r = as_device(e, k_rows, bytes, &e->stage_a, &e->stage_a_bytes, st, &dk);
+    if (r != PE_OK) return r;
+    r = as_device(e, v_rows, bytes, &e->stage_b, &e->stage_b_bytes, st, &dv);
+    if (r != PE_OK) return r;
+    r = as_device(e, positions, sizeof(int64_t) * s.n_seqs, &e->stage_c, &e->stage_c_bytes, st, &dp);
+    if (r != PE_OK) return r;
+    plan_kernel<<<1, 1024, 0, st>>>(s, ts, kPlanAppend, e->rank, nullptr, nullptr, e->ctl);
+    const int warps = kAppendThreads / 32;
+    const int blocks = (n + 16 * warps - 1) / (16 * warps);
+    append_kernel<<<blocks, kAppendThreads, warps * 2 * kStageBytes, st>>>(
+        s, ts, dk, dv, reinterpret_cast<const int64_t*>(dp), e->rank, e->ctl);
+    r = check_launch(e, "append_kernel");
+    if (r != PE_OK) return r;
+    e->stats.kernel_launches += 2;
+    e->stats.append_calls += 1;
+    return PE_OK;
+}
+
+// ------------------------------------------------------------------ K2 / K2c
+pe_status pe_decode_evict(pe_engine* e, int32_t layer_begin, int32_t n_layers, int64_t step,
+                          int32_t mode, int32_t* victims, void* stream) {
+    (void)step;
+    if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
+    const DevState& s = e->s;
+    if (layer_begin < 0 || n_layers <= 0 || layer_begin + n_layers > s.n_layers)
+        return fail(PE_INVALID_ARG, "layer range out of range");
+    if (mode != PE_SCORE_RECOMPUTE && mode != PE_SCORE_CACHED) return fail(PE_INVALID_ARG, "score mode");
+    cudaSetDevice(e->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TableSet ts{layer_begin, n_layers};
+    const int n = ts.size(s);
+    const bool vic_dev = victims && is_device_ptr(victims);
+    int32_t* vdst = vic_dev ? victims : e->victims;
+    plan_kernel<<<1, 1024, 0, st>>>(s, ts, kPlanEvict, e->rank, e->work, vdst, e->ctl);
+    const int ymax = n;
+    if (mode == PE_SCORE_RECOMPUTE) {
+        const int chunks = (s.max_pages + kEvictPagesPerCta - 1) / kEvictPagesPerCta;
+        const int smem = (kEvictThreads / 32) * kEvictStages * kStageBytes;
+        evict_score_kernel<<<dim3(ymax, chunks), kEvictThreads, smem, st>>>(
+            s, ts, kEvictPagesPerCta, e->work, e->rank, e->ctl, e->evict_scratch, e->tickets, vdst);
+    } else {
+        evict_cached_kernel<<<(ymax + 7) / 8, 256, 0, st>>>(s, ts, e->work, e->rank, e->ctl,
+                                                           e->evict_scratch, vdst);
+    }
+    pe_status r = check_launch(e, "evict kernel");
+    if (r != PE_OK) return r;
+    e->stats.kernel_launches += 2;
+    e->stats.evict_calls += 1;
+    if (victims && !vic_dev) {
+        PE_CUDA(cudaMemcpyAsync(victims, e->victims, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    }
+    return PE_OK;
+}
+
+pe_status pe_decode_step(pe_engine* e, int32_t layer_begin, int32_t n_layers, const void* k_rows,
+                         const void* v_rows, const int64_t* positions, int64_t step, int32_t mode,
+                         int32_t* victims, void* stream) {
+    pe_status r = pe_decode_append(e, layer_begin, n_layers, k_rows, v_rows, positions, stream);
+    if (r != PE_OK) return r;
+    return pe_decode_evict(e, layer_begin, n_layers, step, mode, victims, stream);
+}
+
+// ------------------------------------------------------------------ K3
+pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, float* out,
+                                    int32_t n_q_heads, void* stream) {
+    if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
+    const DevState& s = e->s;
+    if (e->cfg.granularity != PE_GRANULARITY_PER_KV_HEAD)
+        return fail(PE_INVALID_ARG, "attention requires PER_KV_HEAD tables");
+    if (layer < 0 || layer >= s.n_layers) return fail(PE_INVALID_ARG, "layer out of range");
+    if (n_q_heads <= 0 || n_q_heads % s.tab_heads != 0)
+        return fail(PE_LENGTH_MISMATCH, "query heads must be a multiple of KV heads");
+    const int G = n_q_heads / s.tab_heads;
+    if (G > 8) return fail(PE_INVALID_ARG, "at most 8 query heads per KV head");
+    if (s.w > 256) return fail(PE_INVALID_ARG, "head_dim > 256 unsupported");
+    cudaSetDevice(e->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int n_tab = s.n_seqs * s.tab_heads;
+    const uint8_t* dq = nullptr;
+    pe_status r = as_device(e, q, (size_t)s.n_seqs * n_q_heads * s.row_bytes, &e->stage_a,
+                            &e->stage_a_bytes, st, &dq);
+    if (r != PE_OK) return r;
+    int splits = std::max(1, (e->sm_count * 8 + n_tab - 1) / n_tab);
+    splits = std::min(splits, std::max(1, (s.max_pages + 3) / 4));
+    const int pps = (s.max_pages + splits - 1) / splits;
+    splits = (s.max_pages + pps - 1) / pps;
+    r = ensure_t(&e->part_o, &e->part_o_elems, (size_t)n_tab * splits * G * s.w);
+    if (r != PE_OK) return r;
+    r = ensure_t(&e->part_ml, &e->part_ml_elems, (size_t)n_tab * splits * G * 2);
+    if (r != PE_OK) return r;
+    const bool out_dev = is_device_ptr(out);
+    const size_t out_elems = (size_t)s.n_seqs * n_q_heads * s.w;
+    if (!out_dev) {
+        r = ensure_t(&e->out_stage, &e->out_stage_elems, out_elems);
+        if (r != PE_OK) return r;
+    }
+    AttnArgs a{};
+    a.q = dq;
+    a.out = out_dev ? out : e->out_stage;
+    a.part_o = e->part_o;
+    a.part_ml = e->part_ml;
+    a.layer = layer;
+    a.G = G;
+    a.n_q_heads = n_q_heads;
+    a.splits = splits;
+    a.pages_per_split = pps;
+    a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(s.w)));
+    const int nw = 4;
+    size_t smem = (size_t)G * s.w * 4 + (size_t)nw * G * 16 * 4 + (size_t)nw * G * s.w * 4 +
+                  (size_t)nw * G * 2 * 4 + 16 + (size_t)nw * 2 * (2 * s.B * (s.row_bytes + 16));
+    if (smem > 227 * 1024) return fail(PE_INVALID_ARG, "attention tile exceeds shared memory");
+    attention_split_kernel<<<dim3(splits, n_tab), 128, smem, st>>>(s, a);
+    attention_merge_kernel<<<n_tab, 128, 0, st>>>(s, a);
+    r = check_launch(e, "attention");
+    if (r != PE_OK) return r;
+    e->stats.kernel_launches += 2;
+    e->stats.attention_calls += 1;
+    if (!out_dev) {
+        PE_CUDA(cudaMemcpyAsync(out, e->out_stage, sizeof(float) * out_elems, cudaMemcpyDeviceToHost, st));
+    }
+    return PE_OK;
+}
+
+// ------------------------------------------------------------------ sync / readback
+pe_status pe_sync(pe_engine* e) {
+    if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
+    cudaSetDevice(e->device);
+    PE_CUDA(cudaDeviceSynchronize());
+    int32_t st = 0;
+    PE_CUDA(cudaMemcpy(&st, e->s.status, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (st != 0) {
+        PE_CUDA(cudaMemset(e->s.status, 0, sizeof(int32_t)));
+        return fail(static_cast<pe_status>(st), pe_status_string(static_cast<pe_status>(st)));
+    }
+    return PE_OK;
+}
+
+pe_status pe_get_info(pe_engine* e, pe_info* out) {
+    if (e == nullptr || out == nullptr) return fail(PE_INVALID_ARG, "null argument");
+    const DevState& s = e->s;
+    cudaSetDevice(e->device);
+    std::memset(out, 0, sizeof(*out));
+    out->n_tables = s.n_tables;
+    out->tab_heads = s.tab_heads;
+    out->width = s.w;
+    out->page_size = s.B;
+    out->cache_budget = s.C;
+    out->capacity = s.capacity;
+    out->max_pages = s.max_pages;
+    out->dtype = s.dtype;
+    out->policy = s.policy;
+    out->granularity = e->cfg.granularity;
+    out->row_pitch_bytes = s.pitch;
+    out->sm_count = e->sm_count;
+    out->pool_bytes = (int64_t)s.capacity * 2 * s.B * s.pitch;
+    out->state_bytes = (int64_t)s.capacity * s.B * 12 + (int64_t)s.capacity * 12 +
+                       (int64_t)s.n_tables * (s.max_pages + 3) * 4;
+    PE_CUDA(cudaDeviceSynchronize());
+    PE_CUDA(cudaMemcpy(&out->free_pages, s.top, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    return PE_OK;
+}
+
+pe_status pe_get_stats(pe_engine* e, pe_stats* out) {
+    if (e == nullptr || out == nullptr) return fail(PE_INVALID_ARG, "null argument");
+    cudaSetDevice(e->device);
+    *out = e->stats;
+    unsigned long long ev = 0;
+    PE_CUDA(cudaDeviceSynchronize());
+    PE_CUDA(cudaMemcpy(&ev, e->s.evict_count, sizeof(ev), cudaMemcpyDeviceToHost));
+    out->pages_evicted = static_cast<int64_t>(ev);
+    return PE_OK;
+}
+
+pe_status pe_read_tables(pe_engine* e, int32_t* block_table, int32_t* num_pages, int32_t* newest_fill,
+                         int32_t* retained) {
+    if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
+    const DevState& s = e->s;
+    cudaSetDevice(e->device);
+    PE_CUDA(cudaDeviceSynchronize());
+    if (block_table)
+        PE_CUDA(cudaMemcpy(block_table, s.block_table, sizeof(int32_t) * (size_t)s.n_tables * s.max_pages,
+                           cudaMemcpyDeviceToHost));
+    if (num_pages) PE_CUDA(cudaMemcpy(num_pages, s.num_pages, sizeof(int32_t) * s.n_tables, cudaMemcpyDeviceToHost));
+    if (newest_fill)
+        PE_CUDA(cudaMemcpy(newest_fill, s.newest_fill, sizeof(int32_t) * s.n_tables, cudaMemcpyDeviceToHost));
+    if (retained) PE_CUDA(cudaMemcpy(retained, s.retained, sizeof(int32_t) * s.n_tables, cudaMemcpyDeviceToHost));
+    return PE_OK;
+}
+
+pe_status pe_read_free_list(pe_engine* e, int32_t* stack_out, int32_t* n_free) {
+    if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
+    cudaSetDevice(e->device);
+    PE_CUDA(cudaDeviceSynchronize());
+    int32_t top = 0;
+    PE_CUDA(cudaMemcpy(&top, e->s.top, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (n_free) *n_free = top;
+    if (stack_out && top > 0)
+        PE_CUDA(cudaMemcpy(stack_out, e->s.stack, sizeof(int32_t) * top, cudaMemcpyDeviceToHost));
+    return PE_OK;
+}
+
+pe_status pe_read_positions(pe_engine* e, int32_t page_begin, int32_t n_pages, int32_t* positions,
+                            double* token_scores, double* page_scores) {
+    if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
+    const DevState& s = e->s;
+    if (page_begin < 0 || n_pages < 0 || page_begin + n_pages > s.capacity)
+        return fail(PE_INDEX_OUT_OF_RANGE, "page range out of range");
+    cudaSetDevice(e->device);
+    PE_CUDA(cudaDeviceSynchronize());
+    if (positions)
+        PE_CUDA(cudaMemcpy(positions, s.positions + (size_t)page_begin * s.B, sizeof(int32_t) * (size_t)n_pages * s.B,
+                           cudaMemcpyDeviceToHost));
+    if (token_scores)
+        PE_CUDA(cudaMemcpy(token_scores, s.token_scores + (size_t)page_begin * s.B,
+                           sizeof(double) * (size_t)n_pages * s.B, cudaMemcpyDeviceToHost));
+    if (page_scores)
+        PE_CUDA(cudaMemcpy(page_scores, s.page_scores + page_begin, sizeof(double) * n_pages, cudaMemcpyDeviceToHost));
+    return PE_OK;
+}
+
+pe_status pe_read_pages(pe_engine* e, int32_t page_begin, int32_t n_pages, void* out) {
+    if (e == nullptr || out == nullptr) return fail(PE_INVALID_ARG, "null argument");
+    const DevState& s = e->s;
+    if (page_begin < 0 || n_pages < 0 || page_begin + n_pages > s.capacity)
+        return fail(PE_INDEX_OUT_OF_RANGE, "page range out of range");
+    cudaSetDevice(e->device);
+    PE_CUDA(cudaDeviceSynchronize());
+    const size_t pb = (size_t)2 * s.B * s.pitch;
+    PE_CUDA(cudaMemcpy(out, s.pages + (size_t)page_begin * pb, pb * n_pages, cudaMemcpyDeviceToHost));
+    return PE_OK;
+}
+
+pe_status pe_get_device_view(pe_engine* e, pe_device_view* out) {
+    if (e == nullptr || out == nullptr) return fail(PE_INVALID_ARG, "null argument");
+    out->pages = e->s.pages;
+    out->block_table = e->s.block_table;
+    out->num_pages = e->s.num_pages;
+    out->newest_fill = e->s.newest_fill;
+    out->retained = e->s.retained;
+    out->positions = e->s.positions;
+    return PE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// Kernel declarations and launch constants shared by the kernels and the
+// host side of the engine.
+#pragma once
+
+#include "pe_internal.cuh"
+
+namespace pe {
+
+constexpr int kPlanAppend = 0;
+constexpr int kPlanEvict = 1;
+
+constexpr int kAppendThreads = 128;      // 4 warps x 16 tables
+constexpr int kEvictThreads = 128;       // 4 warps per CTA
+constexpr int kEvictStages = 3;          // cp.async ring depth per warp
+constexpr int kMaxPagesPerCta = 64;
+constexpr int kPrefillThreads = 128;     // 4 warps per CTA
+constexpr int kPrefillStages = 2;
+constexpr int kPrefillCluster = 8;       // CTAs per table (portable cluster size)
+
+struct PrefillArgs {
+    const uint8_t* k;
+    const uint8_t* v;
+    int64_t token_stride;                // bytes between consecutive tokens of one table
+    const int32_t* tab_len;              // [n_tab] L per launch table
+    const int64_t* tab_tok0;             // [n_tab] first token index (cu_seqlens[s])
+    const int32_t* tab_pagebase;         // [n_tab] exclusive prefix of pages popped
+    int32_t* evicted_counts;             // [n_tab] or nullptr
+    int32_t n_tab;
+    int32_t seq_begin, layer;
+    int32_t chunk_cap;                   // max tokens per CTA (keys smem capacity)
+};
+
+__global__ void plan_kernel(DevState s, TableSet ts, int mode, int32_t* rank, int32_t* work,
+                            int32_t* victims, LaunchCtl* ctl);
+__global__ void append_kernel(DevState s, TableSet ts, const uint8_t* k_rows, const uint8_t* v_rows,
+                              const int64_t* positions, const int32_t* rank, const LaunchCtl* ctl);
+__global__ void evict_score_kernel(DevState s, TableSet ts, int pages_per_cta, const int32_t* work,
+                                   const int32_t* rank, const LaunchCtl* ctl, double* scratch,
+                                   int32_t* tickets, int32_t* victims);
+__global__ void evict_cached_kernel(DevState s, TableSet ts, const int32_t* work,
+                                    const int32_t* rank, const LaunchCtl* ctl, double* scratch,
+                                    int32_t* victims);
+__global__ void plan_prefill_kernel(DevState s, PrefillArgs a, int32_t total_pages, LaunchCtl* ctl);
+__global__ void prefill_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
+
+struct AttnArgs {
+    const uint8_t* q;        // [n_seqs][n_q_heads][d]
+    float* out;              // [n_seqs][n_q_heads][d]
+    float* part_o;           // [n_tab][splits][G][d] split partial outputs
+    float* part_ml;          // [n_tab][splits][G][2]  (max, sum)
+    int32_t layer, G, n_q_heads, splits, pages_per_split;
+    float scale_log2;        // log2(e)/sqrt(d)
+};
+__global__ void attention_split_kernel(DevState s, AttnArgs a);
+__global__ void attention_merge_kernel(DevState s, AttnArgs a);
+
+}  // namespace pe

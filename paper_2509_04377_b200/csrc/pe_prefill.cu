@@ -1,0 +1,312 @@
+// K1: fused prefill prune+pack, one thread-block cluster (8 CTAs) per table.
+//
+// Reference path (proj/core/): make_kv norms (kv_vector.hpp:36-48) ->
+// EvictionPolicy::prefill_compress (policy.cpp:54-63) -> compress_by_score
+// (policy.cpp:90-101): token_importance (importance.cpp:11-13) for every
+// token, rank_tokens(k = L - C) (importance.cpp:41-60: k lowest by
+// (score asc, position asc)), drop_positions (policy.cpp:75-86: survivors
+// keep position order) -> append_token of every survivor
+// (block_table.cpp:10-19, LIFO allocate page_pool.cpp:24-33).
+//
+// Device formulation:
+//  1. score   — CTA r of the cluster streams tokens [L*r/8, L*(r+1)/8) of the
+//               table (K and V rows, 16 tokens per warp step) through the exact
+//               fp64 row streamer; key = IEEE bits of S (S >= +0 so the u64
+//               order is the double order), kept in shared memory.
+//  2. select  — cluster-wide MSB radix select (8-bit digits, histograms merged
+//               through DSMEM) of the E-th smallest key: every key with a
+//               smaller prefix is evicted; among keys equal to the final
+//               prefix, the first k_rem in position order (the reference's
+//               position tie rule).
+//  3. compact — block scans + a DSMEM exchange of per-CTA counts give each
+//               survivor its global rank q (position order).
+//  4. pack    — survivor q goes to slot q%B of the table's (q/B)-th page; the
+//               pages are the free-stack entries reserved in canonical order
+//               by plan_prefill_kernel. Token scores and positions are stored
+//               beside the page; full pages get their mean score cached.
+#include <cooperative_groups.h>
+
+#include "pe_kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pe {
+
+__global__ void __launch_bounds__(1024) plan_prefill_kernel(DevState s, PrefillArgs a,
+                                                             int32_t total_pages, LaunchCtl* ctl) {
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.n_tab; i += blockDim.x) {
+        const int h = i % s.tab_heads;
+        const int seq = a.seq_begin + i / s.tab_heads;
+        const int t = (seq * s.n_layers + a.layer) * s.tab_heads + h;
+        if (s.num_pages[t] != 0) atomicOr(&bad, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int top = *s.top;
+        if (bad) {
+            set_status(s.status, PE_INVALID_STATE);
+            ctl->abort = 1;
+        } else if (total_pages > top) {
+            set_status(s.status, PE_POOL_EXHAUSTED);
+            ctl->abort = 1;
+        } else {
+            ctl->abort = 0;
+            ctl->pop_base = top;
+            *s.top = top - total_pages;
+        }
+    }
+}
+
+__global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPrefillThreads)
+    prefill_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint32_t hist[2][256];
+    __shared__ uint32_t tot[256];
+    __shared__ int scan_sm[33];
+    __shared__ int xchg[2];
+    __shared__ int bc[8];
+    __shared__ unsigned long long prefix_sh;
+
+    if (ctl->abort) return;  // uniform for the whole grid
+    const int CL = kPrefillCluster;
+    const int r = static_cast<int>(cluster.block_rank());
+    const int i = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    const int lane = tid & 31;
+    const int wid = tid >> 5;
+    const int nw = nthr >> 5;
+
+    const int L = a.tab_len[i];
+    const int keep = (s.policy == PE_POLICY_PAGED_EVICTION && L > s.C) ? s.C : L;
+    const int E = L - keep;
+    const int lo = static_cast<int>((int64_t)L * r / CL);
+    const int hi = static_cast<int>((int64_t)L * (r + 1) / CL);
+    const int n = hi - lo;
+    const int h = i % s.tab_heads;
+    const int seq = a.seq_begin + i / s.tab_heads;
+    const int t = (seq * s.n_layers + a.layer) * s.tab_heads + h;
+    const int64_t row0 = (a.tab_tok0[i] * s.tab_heads + h) * (int64_t)s.row_bytes;
+    const uint8_t* kbase = a.k + row0;
+    const uint8_t* vbase = a.v + row0;
+
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
+    const int keys_bytes = ((a.chunk_cap * 8) + 15) & ~15;
+    uint8_t* stage_all = smem + keys_bytes;
+    int32_t* list = reinterpret_cast<int32_t*>(stage_all);  // reused after phase 1
+
+    // ---------------------------------------------------------------- 1. score
+    {
+        const int n_sets = (n + 15) / 16;
+        const int my_sets = n_sets > wid ? (n_sets - wid + nw - 1) / nw : 0;
+        uint8_t* stage = stage_all + wid * (kPrefillStages * kStageBytes);
+        warp_stream_sumsq<kPrefillStages>(
+            my_sets, s.row_bytes, s.w, s.dtype, stage,
+            [&](int set, int row) -> const uint8_t* {
+                const int tok = lo + (wid + set * nw) * 16 + (row & 15);
+                if (tok >= hi) return nullptr;
+                return (row < 16 ? kbase : vbase) + (int64_t)tok * a.token_stride;
+            },
+            [&](int set, double sq, bool present) {
+                const double v2 = __shfl_down_sync(0xFFFFFFFFu, sq, 16);
+                if (lane < 16 && present) {
+                    const int tok = lo + (wid + set * nw) * 16 + lane;
+                    keys[tok - lo] =
+                        static_cast<unsigned long long>(__double_as_longlong(token_score_from_sumsq(sq, v2)));
+                }
+            });
+    }
+    __syncthreads();
+
+    // ---------------------------------------------------------------- 2. select
+    int k_rem = 0;
+    int final_shift = 64;
+    unsigned long long prefix = 0;
+    if (E > 0) {
+        k_rem = E;
+        int shift = 64;
+        for (int pass = 0; pass < 8; ++pass) {
+            shift -= 8;
+            uint32_t* hb = hist[pass & 1];
+            for (int b = tid; b < 256; b += nthr) hb[b] = 0;
+            __syncthreads();
+            for (int j = tid; j < n; j += nthr) {
+                const unsigned long long key = keys[j];
+                const bool match = (pass == 0) || ((key >> (shift + 8)) == prefix);
+                if (match) atomicAdd(&hb[(key >> shift) & 255u], 1u);
+            }
+            cluster.sync();
+            for (int b = tid; b < 256; b += nthr) {
+                uint32_t acc = 0;
+                for (int rr = 0; rr < CL; ++rr) acc += cluster.map_shared_rank(hb, rr)[b];
+                tot[b] = acc;
+            }
+            __syncthreads();
+            if (wid == 0) {
+                uint32_t part[8];
+                uint32_t lsum = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    part[q] = tot[lane * 8 + q];
+                    lsum += part[q];
+                }
+                const int incl = warp_incl_scan(static_cast<int>(lsum));
+                int cum = incl - static_cast<int>(lsum);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (cum < k_rem && k_rem <= cum + static_cast<int>(part[q])) {
+                        bc[0] = lane * 8 + q;
+                        bc[1] = cum;
+                    }
+                    cum += static_cast<int>(part[q]);
+                }
+            }
+            __syncthreads();
+            const int d = bc[0];
+            k_rem -= bc[1];
+            prefix = (prefix << 8) | static_cast<unsigned long long>(d);
+            final_shift = shift;
+            const bool done = static_cast<int>(tot[d]) == k_rem;
+            __syncthreads();
+            if (done) break;
+        }
+    }
+    (void)prefix_sh;
+
+    // ---------------------------------------------------------------- 3. compact
+    auto classify = [&](unsigned long long key, bool& less, bool& tie) {
+        if (E == 0) {
+            less = false;
+            tie = false;
+            return;
+        }
+        const unsigned long long top = key >> final_shift;
+        less = top < prefix;
+        tie = top == prefix;
+    };
+    const int seg = (n + nthr - 1) / nthr;
+    const int a0 = min(n, tid * seg);
+    const int a1 = min(n, a0 + seg);
+    int less_t = 0, tie_t = 0;
+    for (int j = a0; j < a1; ++j) {
+        bool l, tt;
+        classify(keys[j], l, tt);
+        less_t += l;
+        tie_t += tt;
+    }
+    int less_cta, tie_cta;
+    block_excl_scan(less_t, scan_sm, &less_cta);
+    const int tie_before = block_excl_scan(tie_t, scan_sm, &tie_cta);
+    if (tid == 0) {
+        xchg[0] = less_cta;
+        xchg[1] = tie_cta;
+    }
+    cluster.sync();
+    if (tid == 0) {
+        int tie_base = 0, surv_base = 0, kept_me = 0, tb = 0;
+        for (int rr = 0; rr < CL; ++rr) {
+            const int* rx = cluster.map_shared_rank(xchg, rr);
+            const int l_rr = rx[0];
+            const int t_rr = rx[1];
+            const int n_rr = static_cast<int>((int64_t)L * (rr + 1) / CL - (int64_t)L * rr / CL);
+            const int ev_ties = max(0, min(k_rem - tb, t_rr));
+            const int kept = n_rr - l_rr - ev_ties;
+            if (rr < r) {
+                tie_base += t_rr;
+                surv_base += kept;
+            }
+            if (rr == r) kept_me = kept;
+            tb += t_rr;
+        }
+        bc[2] = tie_base;
+        bc[3] = surv_base;
+        bc[4] = kept_me;
+    }
+    __syncthreads();
+    const int tie_base = bc[2];
+    const int surv_base = bc[3];
+    const int kept_me = bc[4];
+    const int my_tie0 = tie_base + tie_before;
+    const int ev_ties_t = max(0, min(k_rem - my_tie0, tie_t));
+    const int keep_t = (a1 - a0) - less_t - ev_ties_t;
+    int keep_cta;
+    int q_local = block_excl_scan(keep_t, scan_sm, &keep_cta);
+    {
+        int tr = my_tie0;
+        for (int j = a0; j < a1; ++j) {
+            bool l, tt;
+            classify(keys[j], l, tt);
+            const bool evict = l || (tt && tr < k_rem);
+            tr += tt;
+            if (!evict) list[q_local++] = j;
+        }
+    }
+    __syncthreads();
+
+    // ---------------------------------------------------------------- 4. pack
+    const int pop_base = ctl->pop_base;
+    const int pagebase = a.tab_pagebase[i];
+    const int B = s.B;
+    for (int m0 = wid; m0 < kept_me; m0 += nw * 4) {
+        uint4 buf[4];
+        int jj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) jj[u] = (m0 + u * nw < kept_me) ? list[m0 + u * nw] : -1;
+        for (int off = (lane & 15) * 16; off < s.row_bytes; off += 256) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (jj[u] >= 0) {
+                    const uint8_t* src = (lane < 16 ? kbase : vbase) + (int64_t)(lo + jj[u]) * a.token_stride;
+                    buf[u] = __ldcs(reinterpret_cast<const uint4*>(src + off));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (jj[u] >= 0) {
+                    const int q = surv_base + m0 + u * nw;
+                    const int page = s.stack[pop_base - 1 - (pagebase + q / B)];
+                    uint8_t* dst = s.pages + (((int64_t)page * 2 + (lane >> 4)) * B + q % B) * s.pitch;
+                    *reinterpret_cast<uint4*>(dst + off) = buf[u];
+                }
+            }
+        }
+        if (lane < 4 && jj[lane] >= 0) {
+            const int u = lane;
+            const int q = surv_base + m0 + u * nw;
+            const int page = s.stack[pop_base - 1 - (pagebase + q / B)];
+            s.positions[(int64_t)page * B + q % B] = lo + jj[u];
+            s.token_scores[(int64_t)page * B + q % B] = __longlong_as_double(static_cast<long long>(keys[jj[u]]));
+        }
+    }
+    const int n_pages = (keep + B - 1) / B;
+    if (r == 0) {
+        for (int p = tid; p < n_pages; p += nthr) {
+            s.block_table[(int64_t)t * s.max_pages + p] = s.stack[pop_base - 1 - (pagebase + p)];
+        }
+        if (tid == 0) {
+            s.num_pages[t] = n_pages;
+            s.newest_fill[t] = keep - (n_pages - 1) * B;
+            s.retained[t] = keep;
+            if (a.evicted_counts) a.evicted_counts[i] = E;
+        }
+    }
+
+    // ---------------------------------------------------------------- 5. page scores
+    __threadfence();
+    cluster.sync();
+    const int full_pages = keep / B;
+    for (int p = tid; p < full_pages; p += nthr) {
+        const int qlast = p * B + B - 1;
+        if (qlast < surv_base || qlast >= surv_base + kept_me) continue;
+        const int page = s.stack[pop_base - 1 - (pagebase + p)];
+        double sum = 0.0;
+        for (int j = 0; j < B; ++j) sum += __ldcg(s.token_scores + (int64_t)page * B + j);
+        s.page_scores[page] = sum / static_cast<double>(B);
+    }
+}
+
+}  // namespace pe

@@ -1,0 +1,80 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library builds, loads
+without a GPU, exports every symbol include/pe/pe.h declares, and fails
+loudly (PE_NO_DEVICE) instead of falling back to the CPU."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "pe" / "pe.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(pe_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_declares_the_path():
+    fns = declared_functions()
+    for f in ("pe_engine_create", "pe_engine_destroy", "pe_prefill_prune_pack", "pe_decode_append",
+              "pe_decode_evict", "pe_decode_step", "pe_paged_decode_attention", "pe_sync",
+              "pe_read_tables", "pe_read_free_list", "pe_read_positions", "pe_read_pages"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(engine_lib):
+    for name in declared_functions():
+        assert hasattr(engine_lib, name), f"libpe_b200.so does not export {name}"
+
+
+def test_binding_covers_header():
+    from paper_2509_04377_b200 import _lib
+
+    assert set(_lib.SIGNATURES) == set(declared_functions())
+
+
+def test_no_cpu_fallback(engine_lib):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2509_04377_b200 import _lib
+
+    cfg = _lib.PeConfig(n_seqs=1, n_layers=1, n_kv_heads=1, head_dim=8, granularity=0,
+                        page_size=16, cache_budget=64, dtype=0, policy=0, capacity=0,
+                        max_pages_per_table=0, device=0)
+    h = C.c_void_p()
+    st = engine_lib.pe_engine_create(C.byref(cfg), C.byref(h))
+    assert st == 31  # PE_NO_DEVICE
+    assert b"device" in engine_lib.pe_last_error()
+
+
+def test_config_validation_precedes_device_check(engine_lib):
+    from paper_2509_04377_b200 import _lib
+
+    cfg = _lib.PeConfig(n_seqs=1, n_layers=1, n_kv_heads=1, head_dim=8, granularity=0,
+                        page_size=16, cache_budget=1000, dtype=0, policy=0, capacity=0,
+                        max_pages_per_table=0, device=0)
+    h = C.c_void_p()
+    assert engine_lib.pe_engine_create(C.byref(cfg), C.byref(h)) == 9  # BudgetInvalid
+    cfg.cache_budget = 8
+    assert engine_lib.pe_engine_create(C.byref(cfg), C.byref(h)) == 9
+    cfg.cache_budget = 64
+    cfg.head_dim = 3  # 12-byte rows
+    assert engine_lib.pe_engine_create(C.byref(cfg), C.byref(h)) == 20
+
+
+def test_policy_mirror():
+    import paper_2509_04377_b200 as pe
+
+    for kind in pe.PolicyKind:
+        assert pe.parse_policy_kind(pe.to_string(kind)) == kind
+    assert pe.parse_policy_kind("h2o") is None
+    with pytest.raises(pe.BudgetInvalid):
+        pe.PolicyConfig(cache_budget=1000).validate()
+    with pytest.raises(pe.BudgetInvalid):
+        pe.PolicyConfig(cache_budget=8).validate()
+    pe.PolicyConfig(cache_budget=4096).validate()

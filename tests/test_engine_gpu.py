@@ -1,0 +1,264 @@
+"""GPU parity of the CUDA engine against the C oracle (and, for small cases,
+the compiled reference itself), all through the C-ABI.
+
+Bit-exact: block tables, num_pages/newest_fill/retained, the free list,
+positions, page bytes, victims, evicted counts, token and page scores.
+Attention: relative L2 (output_deviation) <= 1e-5 (fp32) / 1e-3 (bf16).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from tests.harness import RefReplay, compare_states, compare_with_reference, grid_kv, oracle_state, random_kv
+
+torch = pytest.importorskip("torch")
+pe = pytest.importorskip("paper_2509_04377_b200")
+
+pytestmark = pytest.mark.gpu
+
+
+def make_pair(*, n_seqs, n_layers, H, d, B, C, dtype, cap=0, max_pages=0, kind=0):
+    geo = pe.EngineGeometry(n_seqs=n_seqs, n_layers=n_layers, n_kv_heads=H, head_dim=d,
+                            dtype=dtype, capacity=cap, max_pages_per_table=max_pages)
+    eng = pe.PagedEvictionEngine(geo, pe.PolicyConfig(cache_budget=C, page_size=B,
+                                                      kind=pe.PolicyKind(kind)))
+    orc = oracle.OracleEngine(n_seqs=n_seqs, n_layers=n_layers, n_tab_heads=H, width=d,
+                              page_size=B, budget=C, dtype=dtype, capacity=eng.capacity,
+                              max_pages=eng.max_pages, policy=kind)
+    return eng, orc
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def check(eng, orc, what="", pages=True):
+    st = eng.state(with_pages=pages)
+    ost = oracle_state(orc)
+    compare_states(st, ost, eng.n_tables, eng.B, check_pages=pages, what=what)
+    # cached scores of every live slot / full page are the oracle's bit for bit
+    for t in range(eng.n_tables):
+        n = int(st["num_pages"][t])
+        for j in range(n):
+            pid = int(st["block_table"][t, j])
+            fill = eng.B if j < n - 1 else int(st["newest_fill"][t])
+            np.testing.assert_array_equal(st["token_scores"][pid, :fill],
+                                          orc.token_scores()[pid, :fill], err_msg=f"{what}token scores")
+            if fill == eng.B:
+                assert st["page_scores"][pid] == ost["page_scores"][pid], f"{what}page score {pid}"
+
+
+@pytest.mark.parametrize("dtype", [oracle.F32, oracle.BF16])
+@pytest.mark.parametrize("gen", [random_kv, grid_kv])
+def test_prefill_parity(dtype, gen):
+    rng = np.random.default_rng(100 + dtype)
+    B, C, d, H = 16, 64, 64 if dtype == oracle.F32 else 128, 2
+    lens = np.array([C + 1, 3 * C + 7, C, 5, 1, 2 * C, 1000])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=len(lens), n_layers=2, H=H, d=d, B=B, C=C, dtype=dtype)
+    for layer in range(2):
+        k, _ = gen(rng, (cu[-1], H, d), dtype)
+        v, _ = gen(rng, (cu[-1], H, d), dtype)
+        ev = eng.prefill_compress(layer, dev(k), dev(v), cu, evicted_counts=True)
+        st, oev = orc.prefill(layer, k, v, cu)
+        assert st == 0
+        np.testing.assert_array_equal(ev, oev)
+    eng.sync()
+    check(eng, orc, "prefill: ")
+
+
+def test_prefill_ties_across_cta_boundaries():
+    """Every token of a table scores identically: the E evicted tokens must be
+    exactly the oldest E (position tie rule, importance.cpp:46-52), even
+    though the ties straddle the 8 CTAs of the cluster."""
+    B, C, d, H = 16, 256, 128, 1
+    L = 2000
+    k = np.tile(oracle.f32_to_bf16_bits(np.full(d, 0.5, np.float32)), (L, H, 1))
+    cu = np.array([0, L], np.int32)
+    eng, orc = make_pair(n_seqs=1, n_layers=1, H=H, d=d, B=B, C=C, dtype=oracle.BF16)
+    eng.prefill_compress(0, dev(k), dev(k), cu)
+    orc.prefill(0, k, k, cu)
+    eng.sync()
+    check(eng, orc, "ties: ")
+    np.testing.assert_array_equal(eng.retained_positions(0), np.arange(L - C, L))
+
+
+@pytest.mark.parametrize("dtype", [oracle.F32, oracle.BF16])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_decode_parity(dtype, mode):
+    rng = np.random.default_rng(7 + 10 * dtype + mode)
+    B, C, H, n_layers, S = 16, 64, 2, 3, 3
+    d = 64 if dtype == oracle.F32 else 128
+    lens = np.array([C + 20, C - 5, 200])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=S, n_layers=n_layers, H=H, d=d, B=B, C=C, dtype=dtype)
+    for layer in range(n_layers):
+        k, _ = random_kv(rng, (cu[-1], H, d), dtype)
+        v, _ = random_kv(rng, (cu[-1], H, d), dtype)
+        eng.prefill_compress(layer, dev(k), dev(v), cu)
+        orc.prefill(layer, k, v, cu)
+    pos = lens.astype(np.int64).copy()
+    for step in range(1, 3 * B + 4):
+        k, _ = random_kv(rng, (n_layers, S, H, d), dtype)
+        v, _ = random_kv(rng, (n_layers, S, H, d), dtype)
+        if step % 3 == 0:  # per-layer launches
+            for layer in range(n_layers):
+                vic = eng.decode_step(layer, 1, dev(k[layer:layer + 1]), dev(v[layer:layer + 1]),
+                                      dev(pos), step, mode=mode, victims=True)
+                assert orc.decode_append(layer, 1, k[layer:layer + 1], v[layer:layer + 1], pos) == 0
+                _, ovic = orc.decode_evict(layer, 1)
+                np.testing.assert_array_equal(vic, ovic, err_msg=f"step {step} layer {layer}")
+        else:
+            vic = eng.decode_step(0, n_layers, dev(k), dev(v), dev(pos), step, mode=mode,
+                                  victims=True)
+            assert orc.decode_append(0, n_layers, k, v, pos) == 0
+            _, ovic = orc.decode_evict(0, n_layers)
+            np.testing.assert_array_equal(vic, ovic, err_msg=f"step {step}")
+        pos += 1
+        if step % 8 == 0:
+            eng.sync()
+            check(eng, orc, f"step {step}: ", pages=(step % 16 == 0))
+    eng.sync()
+    check(eng, orc, "final: ")
+    assert eng.stats().pages_evicted > 0
+
+
+def test_engine_matches_compiled_reference(reference):
+    """Direct replay through the reference's own PagePool/BlockTable/policy."""
+    rng = np.random.default_rng(42)
+    B, C, d, H, S, n_layers = 8, 40, 16, 2, 3, 2
+    lens = np.array([100, 17, 41])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, _ = make_pair(n_seqs=S, n_layers=n_layers, H=H, d=d, B=B, C=C, dtype=oracle.F32)
+    rep = RefReplay(reference, n_seqs=S, n_layers=n_layers, n_tab_heads=H, width=d, page_size=B,
+                    budget=C, capacity=eng.capacity)
+    for layer in range(n_layers):
+        k, _ = grid_kv(rng, (cu[-1], H, d), oracle.F32)
+        v, _ = random_kv(rng, (cu[-1], H, d), oracle.F32)
+        eng.prefill_compress(layer, dev(k), dev(v), cu)
+        rep.prefill(layer, k, v, cu)
+    pos = lens.astype(np.int64).copy()
+    for step in range(1, 30):
+        k, _ = random_kv(rng, (n_layers, S, H, d), oracle.F32)
+        v, _ = grid_kv(rng, (n_layers, S, H, d), oracle.F32)
+        vic = eng.decode_step(0, n_layers, dev(k), dev(v), dev(pos), step, victims=True)
+        np.testing.assert_array_equal(vic, rep.decode(0, n_layers, k, v, pos, step))
+        pos += 1
+    eng.sync()
+    st = eng.state()
+    compare_with_reference(rep, st)
+    np.testing.assert_array_equal(rep.sess.drain_free_list(), st["free_stack"][::-1])
+
+
+@pytest.mark.parametrize("dtype,tol", [(oracle.F32, 1e-5), (oracle.BF16, 1e-3)])
+def test_attention_parity(dtype, tol):
+    rng = np.random.default_rng(9)
+    B, C, H, G = 16, 128, 2, 4
+    d = 64 if dtype == oracle.F32 else 128
+    lens = np.array([300, 50, 128, 7])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=len(lens), n_layers=1, H=H, d=d, B=B, C=C, dtype=dtype)
+    k, _ = random_kv(rng, (cu[-1], H, d), dtype)
+    v, _ = random_kv(rng, (cu[-1], H, d), dtype)
+    eng.prefill_compress(0, dev(k), dev(v), cu)
+    orc.prefill(0, k, v, cu)
+    pos = lens.astype(np.int64).copy()
+    for step in range(1, 20):
+        kk, _ = random_kv(rng, (1, len(lens), H, d), dtype)
+        vv, _ = random_kv(rng, (1, len(lens), H, d), dtype)
+        eng.decode_step(0, 1, dev(kk), dev(vv), dev(pos), step)
+        orc.decode_append(0, 1, kk, vv, pos)
+        orc.decode_evict(0, 1)
+        pos += 1
+        q, _ = random_kv(rng, (len(lens), H * G, d), dtype)
+        out = torch.empty((len(lens), H * G, d), dtype=torch.float32, device="cuda")
+        eng.attend(0, dev(q), out, H * G)
+        _, ref = orc.attention(0, q, G)
+        got = out.cpu().numpy()
+        for s in range(len(lens)):
+            for hq in range(H * G):
+                dev_ = oracle.Oracle().output_deviation(got[s, hq], ref[s, hq])
+                assert dev_ <= tol, f"step {step} seq {s} head {hq}: deviation {dev_}"
+
+
+def test_host_buffers_match_device_buffers():
+    rng = np.random.default_rng(3)
+    B, C, d, H = 16, 64, 128, 2
+    lens = np.array([150, 90])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    a, _ = make_pair(n_seqs=2, n_layers=1, H=H, d=d, B=B, C=C, dtype=oracle.BF16)
+    b, _ = make_pair(n_seqs=2, n_layers=1, H=H, d=d, B=B, C=C, dtype=oracle.BF16)
+    k, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+    v, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+    a.prefill_compress(0, dev(k), dev(v), cu)
+    b.prefill_compress(0, k, v, cu)  # numpy host buffers
+    pos = lens.astype(np.int64)
+    for step in range(1, 18):
+        kk, _ = random_kv(rng, (1, 2, H, d), oracle.BF16)
+        vv, _ = random_kv(rng, (1, 2, H, d), oracle.BF16)
+        va = a.decode_step(0, 1, dev(kk), dev(vv), dev(pos), step, victims=True)
+        vb = b.decode_step(0, 1, kk, vv, pos, step, victims=True)
+        np.testing.assert_array_equal(va, vb)
+        pos = pos + 1
+    a.sync()
+    b.sync()
+    compare_states(a.state(), b.state(), a.n_tables, B)
+
+
+def test_error_statuses():
+    # PolicyConfig::validate -> BudgetInvalid (policy.cpp:38-52)
+    geo = pe.EngineGeometry(n_seqs=1, n_layers=1, n_kv_heads=1, head_dim=8, dtype=oracle.F32)
+    with pytest.raises(pe.BudgetInvalid):
+        pe.PagedEvictionEngine(geo, pe.PolicyConfig(cache_budget=1000, page_size=16))
+    with pytest.raises(pe.BudgetInvalid):
+        pe.PagedEvictionEngine(geo, pe.PolicyConfig(cache_budget=8, page_size=16))
+    # PoolExhausted (page_pool.cpp:26-28): all-or-nothing, status via sync()
+    geo = pe.EngineGeometry(n_seqs=2, n_layers=1, n_kv_heads=1, head_dim=8, dtype=oracle.F32,
+                            capacity=3)
+    eng = pe.PagedEvictionEngine(geo, pe.PolicyConfig(cache_budget=8, page_size=4))
+    k = np.ones((16, 1, 8), np.float32)
+    eng.prefill_compress(0, dev(k), dev(k), np.array([0, 8, 16], np.int32))
+    with pytest.raises(pe.PoolExhausted):
+        eng.sync()
+    assert eng.free_count() == 3
+    # prefill into a non-empty table -> InvalidState
+    eng.prefill_compress(0, dev(k[:8]), dev(k[:8]), np.array([0, 8], np.int32))
+    eng.sync()
+    eng.prefill_compress(0, dev(k[:8]), dev(k[:8]), np.array([0, 8], np.int32))
+    with pytest.raises(pe.InvalidState):
+        eng.sync()
+    # empty prefill -> Error (policy.cpp:57-58)
+    with pytest.raises(pe.Error):
+        eng.prefill_compress(0, dev(k), dev(k), np.array([0, 0], np.int32), seq_begin=1)
+    # GQA shape mismatch -> LengthMismatch
+    out = torch.empty((2, 3, 8), dtype=torch.float32, device="cuda")
+    with pytest.raises(pe.LengthMismatch):
+        eng.attend(0, dev(np.ones((2, 3, 8), np.float32)), out, 3)
+
+
+@pytest.mark.slow
+def test_cfg1_full_parity():
+    """BASELINE config 1 in full: Llama-3.2-1B KV geometry (16 layers, 8 KV
+    heads, d=64), fp32, 1 sequence of 4096 tokens, C=1024, B=16: prefill all
+    layers, then 64 decode steps (4 triggers per table), recompute eviction."""
+    rng = np.random.default_rng(20250905)
+    eng, orc = make_pair(n_seqs=1, n_layers=16, H=8, d=64, B=16, C=1024, dtype=oracle.F32)
+    cu = np.array([0, 4096], np.int32)
+    for layer in range(16):
+        k, _ = random_kv(rng, (4096, 8, 64), oracle.F32)
+        v, _ = random_kv(rng, (4096, 8, 64), oracle.F32)
+        eng.prefill_compress(layer, dev(k), dev(v), cu)
+        orc.prefill(layer, k, v, cu)
+    eng.sync()
+    check(eng, orc, "cfg1 prefill: ", pages=False)
+    pos = np.array([4096], np.int64)
+    for step in range(1, 65):
+        k, _ = random_kv(rng, (16, 1, 8, 64), oracle.F32)
+        v, _ = random_kv(rng, (16, 1, 8, 64), oracle.F32)
+        vic = eng.decode_step(0, 16, dev(k), dev(v), dev(pos), step, victims=True)
+        orc.decode_append(0, 16, k, v, pos)
+        _, ovic = orc.decode_evict(0, 16)
+        np.testing.assert_array_equal(vic, ovic)
+        pos += 1
+    eng.sync()
+    check(eng, orc, "cfg1 decode: ")
