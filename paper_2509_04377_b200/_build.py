@@ -20,7 +20,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libpe_b200.so"
 SOURCES = ["pe_engine.cu", "pe_decode.cu", "pe_prefill.cu", "pe_attention.cu"]
-HEADERS = ["pe_internal.cuh", "pe_kernels.cuh"]
+HEADERS = ["pe_internal.cuh", "pe_kernels.cuh", "pe_score.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

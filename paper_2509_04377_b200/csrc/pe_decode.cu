@@ -5,6 +5,7 @@
 //                        table takes the argmin and evicts (PagedEvictionPolicy::evict)
 //   evict_cached_kernel  K2c: the same decision from page means cached at fill time
 #include "pe_kernels.cuh"
+#include "pe_score.cuh"
 
 namespace pe {
 
@@ -83,68 +84,56 @@ __global__ void __launch_bounds__(1024) plan_kernel(DevState s, TableSet ts, int
 }
 
 // ---------------------------------------------------------------------------
-// append_kernel (K0): one warp per 16 launch tables. Lanes 0-15 stream the K
-// rows and lanes 16-31 the V rows of those tables (exact fp64 norms ->
-// cached token score, kv_vector.hpp:42-43), the warp copies both rows into
-// the newest page's write cursor (Page::write, page.hpp:39-44), opening a
-// page popped in canonical order when needed (block_table.cpp:12-15).
-// When the write fills the page its mean score is cached (importance.cpp:19-30).
+// append_kernel (K0): one warp per 16 launch tables; lane pair r owns table
+// i0 + r. The pair reads the new token's K and V rows once into registers,
+// copies them into the newest page's write cursor (Page::write,
+// page.hpp:39-44) and computes the token's exact score from the same
+// registers (cached norms, kv_vector.hpp:42-43). A page is opened (popped in
+// canonical order) when needed (block_table.cpp:12-15); when the write fills
+// the page its mean score is cached (importance.cpp:19-30).
+template <int SV>
 __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, TableSet ts,
                                                                  const uint8_t* __restrict__ k_rows,
                                                                  const uint8_t* __restrict__ v_rows,
                                                                  const int64_t* __restrict__ positions,
                                                                  const int32_t* __restrict__ rank,
                                                                  const LaunchCtl* __restrict__ ctl) {
-    extern __shared__ __align__(16) uint8_t smem[];
     if (ctl->abort) return;
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int n = ts.size(s);
     const int i0 = (blockIdx.x * (kAppendThreads / 32) + wid) * 16;
     if (i0 >= n) return;
-    uint8_t* stage = smem + wid * (2 * kStageBytes);
-    const int my_i = i0 + (lane & 15);
+    const int my_i = i0 + (lane >> 1);
     const bool has = my_i < n;
+    const int q = lane & 1;
 
-    // Resolve (page, slot) for the lane's table (lanes l and l+16 agree).
-    int t = 0, page = -1, slot = 0;
+    int t = 0, page = 0, slot = 0, np = 0, rk = -1;
     if (has) {
         t = ts.table(s, my_i);
-        const int np = s.num_pages[t];
-        if (rank[my_i] >= 0) {
-            page = s.stack[ctl->pop_base - 1 - rank[my_i]];
+        np = s.num_pages[t];
+        rk = rank[my_i];
+        if (rk >= 0) {
+            page = s.stack[ctl->pop_base - 1 - rk];
             slot = 0;
-            if (lane < 16) {
-                s.block_table[(int64_t)t * s.max_pages + np] = page;
-                s.num_pages[t] = np + 1;
-            }
         } else {
             page = s.block_table[(int64_t)t * s.max_pages + np - 1];
             slot = s.newest_fill[t];
         }
     }
-    const int64_t in_row = has ? ts.input_row(s, my_i) : 0;
-    const uint8_t* src = (lane < 16 ? k_rows : v_rows) + in_row * s.row_bytes;
-
-    // copy: each half-warp lane copies its row (row_bytes multiple of 16)
-    if (has) {
-        uint8_t* dst = s.pages + (((int64_t)page * 2 + (lane >> 4)) * s.B + slot) * s.pitch;
-        for (int off = 0; off < s.row_bytes; off += 16) {
-            *reinterpret_cast<uint4*>(dst + off) = __ldg(reinterpret_cast<const uint4*>(src + off));
-        }
+    __syncwarp();  // both lanes of a pair read the table state before lane 0 updates it
+    if (has && q == 0 && rk >= 0) {
+        s.block_table[(int64_t)t * s.max_pages + np] = page;
+        s.num_pages[t] = np + 1;
     }
-    // exact norms via the warp streamer (one set of 32 rows)
-    double sq = 0.0;
-    warp_stream_sumsq<2>(1, s.row_bytes, s.w, s.dtype, stage,
-                         [&](int, int row) -> const uint8_t* {
-                             const int ii = i0 + (row & 15);
-                             if (ii >= n) return nullptr;
-                             return (row < 16 ? k_rows : v_rows) + ts.input_row(s, ii) * s.row_bytes;
-                         },
-                         [&](int, double r, bool) { sq = r; });
-    const double v2 = __shfl_down_sync(0xFFFFFFFFu, sq, 16);
-    if (has && lane < 16) {
-        const double S = token_score_from_sumsq(sq, v2);
+    const int64_t in_row = has ? ts.input_row(s, my_i) : 0;
+    const uint8_t* krow = k_rows + in_row * s.row_bytes;
+    const uint8_t* vrow = v_rows + in_row * s.row_bytes;
+    uint8_t* kdst = s.pages + (((int64_t)page * 2 + 0) * s.B + slot) * s.pitch;
+    uint8_t* vdst = s.pages + (((int64_t)page * 2 + 1) * s.B + slot) * s.pitch;
+    const double S = pair_token_score<SV>(krow, vrow, has, s.w, s.dtype, has ? kdst : nullptr,
+                                          has ? vdst : nullptr);
+    if (has && q == 0) {
         const int64_t ps = (int64_t)page * s.B + slot;
         s.positions[ps] = static_cast<int32_t>(positions[ts.input_row(s, my_i) / s.tab_heads % s.n_seqs]);
         s.token_scores[ps] = S;
@@ -212,16 +201,16 @@ __device__ __forceinline__ void finalize_evict(const DevState& s, int t, int i, 
 
 // ---------------------------------------------------------------------------
 // evict_score_kernel (K2, recompute): grid (work items, chunks). CTA (y, c)
-// scores pages [c*P, c*P+P) of evicting table work[y]: warps stream whole
-// pages (2B contiguous rows: K slots then V slots) through the exact fp64
-// row streamer, S per slot = ||V||/max(||K||,eps), page mean = slot-order sum
-// / fill (score_pages -> page_score, importance.cpp:19-39). The last CTA of
-// the table (atomic ticket) takes the argmin and evicts.
-__global__ void __launch_bounds__(kEvictThreads) evict_score_kernel(
+// scores pages [c*P, c*P+P) of evicting table work[y]; each warp takes whole
+// pages: lane pair r scores slot r (K row r, V row r of the page, both
+// 256-byte rows read straight into registers), the page mean is the
+// slot-order sum / fill (score_pages -> page_score, importance.cpp:19-39).
+// The last CTA of the table (atomic ticket) takes the argmin and evicts.
+template <int SV>
+__global__ void __launch_bounds__(kEvictThreads, 3) evict_score_kernel(
     DevState s, TableSet ts, int pages_per_cta, const int32_t* __restrict__ work,
     const int32_t* __restrict__ rank, const LaunchCtl* __restrict__ ctl, double* scratch,
     int32_t* tickets, int32_t* victims) {
-    extern __shared__ __align__(16) uint8_t smem[];
     __shared__ double page_mean[kMaxPagesPerCta];
     __shared__ int last;
     const int y = blockIdx.x;
@@ -238,34 +227,22 @@ __global__ void __launch_bounds__(kEvictThreads) evict_score_kernel(
     const int wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
     const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
-    const int sets_per_page = (s.B + 15) / 16;
-    uint8_t* stage = smem + wid * (kEvictStages * kStageBytes);
+    const int64_t page_bytes = (int64_t)2 * s.B * s.pitch;
 
-    // this warp's pages: p0 + wid, p0 + wid + nw, ...
-    const int my_pages = np > wid ? (np - wid + nw - 1) / nw : 0;
-    double sum = 0.0;  // running slot-order sum of the current page (lane 0)
-    warp_stream_sumsq<kEvictStages>(
-        my_pages * sets_per_page, s.row_bytes, s.w, s.dtype, stage,
-        [&](int set, int r) -> const uint8_t* {
-            const int pg = p0 + wid + (set / sets_per_page) * nw;
-            const int q = set % sets_per_page;
-            const int slot = q * 16 + (r & 15);
-            if (slot >= s.B) return nullptr;
-            const int id = row[pg];
-            return s.pages + (((int64_t)id * 2 + (r >> 4)) * s.B + slot) * s.pitch;
-        },
-        [&](int set, double sq, bool present) {
-            const double v2 = __shfl_down_sync(0xFFFFFFFFu, sq, 16);
-            double S = 0.0;
-            if (lane < 16 && present) S = token_score_from_sumsq(sq, v2);
-            const int q = set % sets_per_page;
-            const int nslots = min(16, s.B - q * 16);
-            for (int j = 0; j < nslots; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, j);
-            if (q == sets_per_page - 1) {
-                if (lane == 0) page_mean[(set / sets_per_page) * nw + wid] = sum / (double)s.B;
-                sum = 0.0;
-            }
-        });
+    for (int lp = wid; lp < np; lp += nw) {
+        const int id = __ldg(row + p0 + lp);
+        const uint8_t* base = s.pages + (int64_t)id * page_bytes;
+        double sum = 0.0;
+        for (int s0 = 0; s0 < s.B; s0 += 16) {
+            const int slot = s0 + (lane >> 1);
+            const bool valid = slot < s.B;
+            const double S = pair_token_score<SV>(base + (int64_t)slot * s.pitch,
+                                                  base + (int64_t)(s.B + slot) * s.pitch, valid, s.w, s.dtype);
+            const int ns = min(16, s.B - s0);
+            for (int j = 0; j < ns; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+        }
+        if (lane == 0) page_mean[lp] = sum / static_cast<double>(s.B);
+    }
     __syncthreads();
     for (int j = threadIdx.x; j < np; j += blockDim.x) {
         scratch[(int64_t)y * s.max_pages + p0 + j] = page_mean[j];
@@ -280,11 +257,35 @@ __global__ void __launch_bounds__(kEvictThreads) evict_score_kernel(
     if (!last) return;
     __threadfence();
     if (wid == 0) {
-        const double* sc = scratch + (int64_t)y * s.max_pages;
-        // volatile-free: other CTAs' writes are ordered by their fence + our ticket
-        finalize_evict(s, t, i, N, sc, rank, ctl, victims, nullptr);
+        finalize_evict(s, t, i, N, scratch + (int64_t)y * s.max_pages, rank, ctl, victims, nullptr);
         if (lane == 0) tickets[y] = 0;
     }
+}
+
+template <int SV>
+void launch_evict_score(dim3 grid, int threads, cudaStream_t st, const DevState& s, const TableSet& ts, int ppc,
+                        const int32_t* work, const int32_t* rank, const LaunchCtl* ctl, double* scratch,
+                        int32_t* tickets, int32_t* victims) {
+    evict_score_kernel<SV><<<grid, threads, 0, st>>>(s, ts, ppc, work, rank, ctl, scratch, tickets, victims);
+}
+
+template <int SV>
+void launch_append(int blocks, cudaStream_t st, const DevState& s, const TableSet& ts, const uint8_t* k,
+                   const uint8_t* v, const int64_t* pos, const int32_t* rank, const LaunchCtl* ctl) {
+    append_kernel<SV><<<blocks, kAppendThreads, 0, st>>>(s, ts, k, v, pos, rank, ctl);
+}
+
+void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st, const DevState& s,
+                            const TableSet& ts, int ppc, const int32_t* work, const int32_t* rank,
+                            const LaunchCtl* ctl, double* scratch, int32_t* tickets, int32_t* victims) {
+    PE_SCORE_DISPATCH(variant, (launch_evict_score<SV>(grid, threads, st, s, ts, ppc, work, rank, ctl, scratch,
+                                                        tickets, victims)));
+}
+
+void launch_append_any(int variant, int blocks, cudaStream_t st, const DevState& s, const TableSet& ts,
+                       const uint8_t* k, const uint8_t* v, const int64_t* pos, const int32_t* rank,
+                       const LaunchCtl* ctl) {
+    PE_SCORE_DISPATCH(variant, (launch_append<SV>(blocks, st, s, ts, k, v, pos, rank, ctl)));
 }
 
 // ---------------------------------------------------------------------------

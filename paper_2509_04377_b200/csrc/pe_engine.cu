@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "pe_kernels.cuh"
+#include "pe_score.cuh"
 
 using namespace pe;
 
@@ -64,6 +65,11 @@ struct pe_engine {
     int64_t* tab_tok0 = nullptr;
     int32_t* tab_pagebase = nullptr;
     int32_t* evicted_dev = nullptr;
+    int64_t* tab_keybase = nullptr;
+    int64_t* h_tab_keybase = nullptr;   // pinned
+    unsigned long long* keys = nullptr;
+    size_t keys_elems = 0;
+    int variant = 0;
     int32_t* h_tab_len = nullptr;       // pinned
     int64_t* h_tab_tok0 = nullptr;      // pinned
     int32_t* h_tab_pagebase = nullptr;  // pinned
@@ -81,6 +87,7 @@ struct pe_engine {
     float* out_stage = nullptr;
     size_t out_stage_elems = 0;
     pe_stats stats{};
+    int max_dyn_prefill = 0, max_dyn_attn = 0;
 };
 
 namespace {
@@ -217,6 +224,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
     e->device = c.device;
     e->sm_count = prop.multiProcessorCount;
     e->tab_heads = tab_heads;
+    e->variant = score_variant(c.dtype, row_bytes);
     DevState& s = e->s;
     s.capacity = static_cast<int32_t>(cap);
     s.B = c.page_size;
@@ -252,14 +260,16 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         dalloc(&e->tab_len, (size_t)c.n_seqs * tab_heads) != cudaSuccess ||
         dalloc(&e->tab_tok0, (size_t)c.n_seqs * tab_heads) != cudaSuccess ||
         dalloc(&e->tab_pagebase, (size_t)c.n_seqs * tab_heads) != cudaSuccess ||
-        dalloc(&e->evicted_dev, (size_t)c.n_seqs * tab_heads) != cudaSuccess) {
+        dalloc(&e->evicted_dev, (size_t)c.n_seqs * tab_heads) != cudaSuccess ||
+        dalloc(&e->tab_keybase, (size_t)c.n_seqs * tab_heads) != cudaSuccess) {
         cudaGetLastError();
         return cleanup_fail(fail(PE_CUDA_ERROR, "device allocation failed (pool of " +
                                                     std::to_string(cap) + " pages)"));
     }
     if (cudaMallocHost(&e->h_tab_len, sizeof(int32_t) * c.n_seqs * tab_heads) != cudaSuccess ||
         cudaMallocHost(&e->h_tab_tok0, sizeof(int64_t) * c.n_seqs * tab_heads) != cudaSuccess ||
-        cudaMallocHost(&e->h_tab_pagebase, sizeof(int32_t) * c.n_seqs * tab_heads) != cudaSuccess) {
+        cudaMallocHost(&e->h_tab_pagebase, sizeof(int32_t) * c.n_seqs * tab_heads) != cudaSuccess ||
+        cudaMallocHost(&e->h_tab_keybase, sizeof(int64_t) * c.n_seqs * tab_heads) != cudaSuccess) {
         cudaGetLastError();
         return cleanup_fail(fail(PE_CUDA_ERROR, "pinned allocation failed"));
     }
@@ -284,12 +294,22 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             return cleanup_fail(fail(PE_CUDA_ERROR, "state initialisation failed"));
         }
     }
-    // kernel attributes (dynamic smem beyond 48 KB)
-    cudaFuncSetAttribute(evict_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (kEvictThreads / 32) * kEvictStages * kStageBytes);
-    cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(attention_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaGetLastError();
+    // kernel attributes: allow dynamic smem up to the opt-in limit minus the static part
+    {
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device);
+        auto allow = [&](const void* fn, int* out) -> bool {
+            cudaFuncAttributes fa{};
+            if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return false;
+            *out = optin - static_cast<int>(fa.sharedSizeBytes);
+            return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, *out) == cudaSuccess;
+        };
+        if (!allow(reinterpret_cast<const void*>(prefill_pack_kernel), &e->max_dyn_prefill) ||
+            !allow(reinterpret_cast<const void*>(attention_split_kernel), &e->max_dyn_attn)) {
+            cudaGetLastError();
+            return cleanup_fail(fail(PE_CUDA_ERROR, "cudaFuncSetAttribute(max dynamic smem) failed"));
+        }
+    }
     *out = e;
     return PE_OK;
 }
@@ -303,13 +323,14 @@ pe_status pe_engine_destroy(pe_engine* e) {
                    s.newest_fill, s.retained, s.stack, s.top, s.status, s.evict_count, e->ctl, e->rank,
                    e->work, e->victims, e->tickets, e->evict_scratch, e->tab_len, e->tab_tok0,
                    e->tab_pagebase, e->evicted_dev, e->stage_a, e->stage_b, e->stage_c, e->part_o,
-                   e->part_ml, e->out_stage};
+                   e->part_ml, e->out_stage, e->tab_keybase, e->keys};
     for (void* p : dev) {
         if (p) cudaFree(p);
     }
     if (e->h_tab_len) cudaFreeHost(e->h_tab_len);
     if (e->h_tab_tok0) cudaFreeHost(e->h_tab_tok0);
     if (e->h_tab_pagebase) cudaFreeHost(e->h_tab_pagebase);
+    if (e->h_tab_keybase) cudaFreeHost(e->h_tab_keybase);
     cudaGetLastError();
     delete e;
     return PE_OK;
@@ -331,6 +352,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     const int H = s.tab_heads;
     const int n_tab = n_seqs * H;
     int64_t total_pages = 0;
+    int64_t total_keys = 0;
     int max_len = 0;
     for (int q = 0; q < n_seqs; ++q) {
         const int L = cu_seqlens[q + 1] - cu_seqlens[q];
@@ -345,13 +367,14 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
             e->h_tab_len[i] = L;
             e->h_tab_tok0[i] = cu_seqlens[q];
             e->h_tab_pagebase[i] = static_cast<int32_t>(total_pages);
+            e->h_tab_keybase[i] = total_keys;
             total_pages += np;
+            total_keys += L;
         }
     }
     const int chunk_cap = (max_len + kPrefillCluster - 1) / kPrefillCluster;
-    const int keys_bytes = ((chunk_cap * 8) + 15) & ~15;
-    const int stage_bytes = (kPrefillThreads / 32) * kPrefillStages * kStageBytes;
-    if (chunk_cap * 4 > stage_bytes || keys_bytes + stage_bytes > 227 * 1024 - 4096)
+    const size_t pack_smem = (size_t)chunk_cap * 12;
+    if (pack_smem > (size_t)e->max_dyn_prefill)
         return fail(PE_INVALID_ARG, "prefill length " + std::to_string(max_len) +
                                         " exceeds the per-cluster shared-memory capacity");
     const size_t tokens = cu_seqlens[n_seqs];
@@ -361,9 +384,12 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     if (r != PE_OK) return r;
     r = as_device(e, v, in_bytes, &e->stage_b, &e->stage_b_bytes, st, &dv);
     if (r != PE_OK) return r;
+    r = ensure_t(&e->keys, &e->keys_elems, (size_t)total_keys);
+    if (r != PE_OK) return r;
     PE_CUDA(cudaMemcpyAsync(e->tab_len, e->h_tab_len, sizeof(int32_t) * n_tab, cudaMemcpyHostToDevice, st));
     PE_CUDA(cudaMemcpyAsync(e->tab_tok0, e->h_tab_tok0, sizeof(int64_t) * n_tab, cudaMemcpyHostToDevice, st));
     PE_CUDA(cudaMemcpyAsync(e->tab_pagebase, e->h_tab_pagebase, sizeof(int32_t) * n_tab, cudaMemcpyHostToDevice, st));
+    PE_CUDA(cudaMemcpyAsync(e->tab_keybase, e->h_tab_keybase, sizeof(int64_t) * n_tab, cudaMemcpyHostToDevice, st));
     const bool ev_dev = evicted_counts && is_device_ptr(evicted_counts);
     PrefillArgs a{};
     a.k = dk;
@@ -373,16 +399,20 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     a.tab_tok0 = e->tab_tok0;
     a.tab_pagebase = e->tab_pagebase;
     a.evicted_counts = evicted_counts ? (ev_dev ? evicted_counts : e->evicted_dev) : nullptr;
+    a.keys = e->keys;
+    a.tab_keybase = e->tab_keybase;
     a.n_tab = n_tab;
     a.seq_begin = seq_begin;
     a.layer = layer;
     a.chunk_cap = chunk_cap;
     if (total_pages > INT32_MAX) return fail(PE_POOL_EXHAUSTED, "page pool exhausted");
     plan_prefill_kernel<<<1, 1024, 0, st>>>(s, a, static_cast<int32_t>(total_pages), e->ctl);
-    prefill_kernel<<<dim3(kPrefillCluster, n_tab), kPrefillThreads, keys_bytes + stage_bytes, st>>>(s, a, e->ctl);
+    launch_prefill_score_any(e->variant, dim3((max_len + kScoreTokensPerCta - 1) / kScoreTokensPerCta, n_tab), st, s,
+                             a, e->ctl);
+    prefill_pack_kernel<<<dim3(kPrefillCluster, n_tab), kPackThreads, pack_smem, st>>>(s, a, e->ctl);
     r = check_launch(e, "prefill_kernel");
     if (r != PE_OK) return r;
-    e->stats.kernel_launches += 2;
+    e->stats.kernel_launches += 3;
     e->stats.prefill_calls += 1;
     e->stats.tokens_scored += (int64_t)tokens * H;
     if (evicted_counts && !ev_dev) {
@@ -413,8 +443,7 @@ pe_status pe_decode_append(pe_engine* e, int32_t layer_begin, int32_t n_layers, 
     plan_kernel<<<1, 1024, 0, st>>>(s, ts, kPlanAppend, e->rank, nullptr, nullptr, e->ctl);
     const int warps = kAppendThreads / 32;
     const int blocks = (n + 16 * warps - 1) / (16 * warps);
-    append_kernel<<<blocks, kAppendThreads, warps * 2 * kStageBytes, st>>>(
-        s, ts, dk, dv, reinterpret_cast<const int64_t*>(dp), e->rank, e->ctl);
+    launch_append_any(e->variant, blocks, st, s, ts, dk, dv, reinterpret_cast<const int64_t*>(dp), e->rank, e->ctl);
     r = check_launch(e, "append_kernel");
     if (r != PE_OK) return r;
     e->stats.kernel_launches += 2;
@@ -441,9 +470,8 @@ pe_status pe_decode_evict(pe_engine* e, int32_t layer_begin, int32_t n_layers, i
     const int ymax = n;
     if (mode == PE_SCORE_RECOMPUTE) {
         const int chunks = (s.max_pages + kEvictPagesPerCta - 1) / kEvictPagesPerCta;
-        const int smem = (kEvictThreads / 32) * kEvictStages * kStageBytes;
-        evict_score_kernel<<<dim3(ymax, chunks), kEvictThreads, smem, st>>>(
-            s, ts, kEvictPagesPerCta, e->work, e->rank, e->ctl, e->evict_scratch, e->tickets, vdst);
+        launch_evict_score_any(e->variant, dim3(ymax, chunks), kEvictThreads, st, s, ts, kEvictPagesPerCta, e->work,
+                               e->rank, e->ctl, e->evict_scratch, e->tickets, vdst);
     } else {
         evict_cached_kernel<<<(ymax + 7) / 8, 256, 0, st>>>(s, ts, e->work, e->rank, e->ctl,
                                                            e->evict_scratch, vdst);
@@ -514,7 +542,7 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
     const int nw = 4;
     size_t smem = (size_t)G * s.w * 4 + (size_t)nw * G * 16 * 4 + (size_t)nw * G * s.w * 4 +
                   (size_t)nw * G * 2 * 4 + 16 + (size_t)nw * 2 * (2 * s.B * (s.row_bytes + 16));
-    if (smem > 227 * 1024) return fail(PE_INVALID_ARG, "attention tile exceeds shared memory");
+    if (smem > (size_t)e->max_dyn_attn) return fail(PE_INVALID_ARG, "attention tile exceeds shared memory");
     attention_split_kernel<<<dim3(splits, n_tab), 128, smem, st>>>(s, a);
     attention_merge_kernel<<<n_tab, 128, 0, st>>>(s, a);
     r = check_launch(e, "attention");

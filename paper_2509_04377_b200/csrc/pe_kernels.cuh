@@ -11,10 +11,10 @@ constexpr int kPlanEvict = 1;
 
 constexpr int kAppendThreads = 128;      // 4 warps x 16 tables
 constexpr int kEvictThreads = 128;       // 4 warps per CTA
-constexpr int kEvictStages = 3;          // cp.async ring depth per warp
 constexpr int kMaxPagesPerCta = 64;
-constexpr int kPrefillThreads = 128;     // 4 warps per CTA
-constexpr int kPrefillStages = 2;
+constexpr int kPrefillThreads = 128;     // score kernel: 4 warps per CTA
+constexpr int kScoreTokensPerCta = 512;  // 4 warps x 8 groups x 16 tokens
+constexpr int kPackThreads = 256;        // select/pack kernel: 8 warps per CTA
 constexpr int kPrefillCluster = 8;       // CTAs per table (portable cluster size)
 
 struct PrefillArgs {
@@ -25,6 +25,8 @@ struct PrefillArgs {
     const int64_t* tab_tok0;             // [n_tab] first token index (cu_seqlens[s])
     const int32_t* tab_pagebase;         // [n_tab] exclusive prefix of pages popped
     int32_t* evicted_counts;             // [n_tab] or nullptr
+    unsigned long long* keys;            // score keys, table i at tab_keybase[i]
+    const int64_t* tab_keybase;          // [n_tab] exclusive prefix of L
     int32_t n_tab;
     int32_t seq_begin, layer;
     int32_t chunk_cap;                   // max tokens per CTA (keys smem capacity)
@@ -32,16 +34,21 @@ struct PrefillArgs {
 
 __global__ void plan_kernel(DevState s, TableSet ts, int mode, int32_t* rank, int32_t* work,
                             int32_t* victims, LaunchCtl* ctl);
-__global__ void append_kernel(DevState s, TableSet ts, const uint8_t* k_rows, const uint8_t* v_rows,
-                              const int64_t* positions, const int32_t* rank, const LaunchCtl* ctl);
-__global__ void evict_score_kernel(DevState s, TableSet ts, int pages_per_cta, const int32_t* work,
-                                   const int32_t* rank, const LaunchCtl* ctl, double* scratch,
-                                   int32_t* tickets, int32_t* victims);
 __global__ void evict_cached_kernel(DevState s, TableSet ts, const int32_t* work,
                                     const int32_t* rank, const LaunchCtl* ctl, double* scratch,
                                     int32_t* victims);
 __global__ void plan_prefill_kernel(DevState s, PrefillArgs a, int32_t total_pages, LaunchCtl* ctl);
-__global__ void prefill_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
+__global__ void prefill_pack_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
+
+// host-side launchers of the row-geometry-specialised kernels (pe_score.cuh variants)
+void launch_append_any(int variant, int blocks, cudaStream_t st, const DevState& s, const TableSet& ts,
+                       const uint8_t* k, const uint8_t* v, const int64_t* pos, const int32_t* rank,
+                       const LaunchCtl* ctl);
+void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st, const DevState& s,
+                            const TableSet& ts, int ppc, const int32_t* work, const int32_t* rank,
+                            const LaunchCtl* ctl, double* scratch, int32_t* tickets, int32_t* victims);
+void launch_prefill_score_any(int variant, dim3 grid, cudaStream_t st, const DevState& s, const PrefillArgs& a,
+                              const LaunchCtl* ctl);
 
 struct AttnArgs {
     const uint8_t* q;        // [n_seqs][n_q_heads][d]

@@ -1,4 +1,4 @@
-// K1: fused prefill prune+pack, one thread-block cluster (8 CTAs) per table.
+// K1: prefill prune+pack — scoring kernel + one thread-block cluster (8 CTAs) per table.
 //
 // Reference path (proj/core/): make_kv norms (kv_vector.hpp:36-48) ->
 // EvictionPolicy::prefill_compress (policy.cpp:54-63) -> compress_by_score
@@ -8,11 +8,13 @@
 // keep position order) -> append_token of every survivor
 // (block_table.cpp:10-19, LIFO allocate page_pool.cpp:24-33).
 //
-// Device formulation:
-//  1. score   — CTA r of the cluster streams tokens [L*r/8, L*(r+1)/8) of the
-//               table (K and V rows, 16 tokens per warp step) through the exact
-//               fp64 row streamer; key = IEEE bits of S (S >= +0 so the u64
-//               order is the double order), kept in shared memory.
+// Device formulation (two kernels):
+//  1. score   — prefill_score_kernel streams every token of every table of the
+//               launch (lane pair per token, exact fp64 certificate scoring,
+//               pe_score.cuh); key = IEEE bits of S (S >= +0 so the u64 order
+//               is the double order), 8 B per token to a key buffer.
+//  select/compact/pack run in prefill_pack_kernel, one cluster of 8 CTAs per
+//  table, CTA r owning tokens [L*r/8, L*(r+1)/8) whose keys it loads to smem:
 //  2. select  — cluster-wide MSB radix select (8-bit digits, histograms merged
 //               through DSMEM) of the E-th smallest key: every key with a
 //               smaller prefix is evicted; among keys equal to the final
@@ -27,6 +29,7 @@
 #include <cooperative_groups.h>
 
 #include "pe_kernels.cuh"
+#include "pe_score.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -60,8 +63,56 @@ __global__ void __launch_bounds__(1024) plan_prefill_kernel(DevState s, PrefillA
     }
 }
 
-__global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPrefillThreads)
-    prefill_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
+// ---------------------------------------------------------------------------
+// prefill_score_kernel: grid (ceil(maxL / 512), n_tab), 4 warps; each warp
+// scores 8 groups of 16 tokens (lane pair per token).
+template <int SV>
+__global__ void __launch_bounds__(kPrefillThreads) prefill_score_kernel(DevState s, PrefillArgs a,
+                                                                         const LaunchCtl* ctl) {
+    if (ctl->abort) return;
+    const int i = blockIdx.y;
+    const int L = a.tab_len[i];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int tok_cta = blockIdx.x * kScoreTokensPerCta;
+    if (tok_cta >= L) return;
+    const int h = i % s.tab_heads;
+    const int64_t row0 = (a.tab_tok0[i] * s.tab_heads + h) * (int64_t)s.row_bytes;
+    const uint8_t* kbase = a.k + row0;
+    const uint8_t* vbase = a.v + row0;
+    unsigned long long* keys = a.keys + a.tab_keybase[i];
+    constexpr int kGroups = kScoreTokensPerCta / 16 / (kPrefillThreads / 32);
+#pragma unroll 1
+    for (int g = 0; g < kGroups; ++g) {
+        const int tok = tok_cta + (wid * kGroups + g) * 16 + (lane >> 1);
+        const bool valid = tok < L;
+        const double S = pair_token_score<SV>(kbase + (int64_t)tok * a.token_stride,
+                                              vbase + (int64_t)tok * a.token_stride, valid, s.w, s.dtype);
+        if (valid && (lane & 1) == 0) keys[tok] = static_cast<unsigned long long>(__double_as_longlong(S));
+    }
+}
+
+template <int SV>
+static void launch_score(dim3 grid, cudaStream_t st, const DevState& s, const PrefillArgs& a, const LaunchCtl* ctl) {
+    prefill_score_kernel<SV><<<grid, kPrefillThreads, 0, st>>>(s, a, ctl);
+}
+
+void launch_prefill_score_any(int variant, dim3 grid, cudaStream_t st, const DevState& s, const PrefillArgs& a,
+                              const LaunchCtl* ctl) {
+    PE_SCORE_DISPATCH(variant, (launch_score<SV>(grid, st, s, a, ctl)));
+}
+
+// Warp-aggregated shared-memory histogram increment (many keys share a
+// digit: S values of one table are concentrated).
+__device__ __forceinline__ void hist_add(uint32_t* hb, uint32_t bin, bool active) {
+    const uint32_t am = __ballot_sync(0xFFFFFFFFu, active);
+    if (!active) return;
+    const uint32_t peers = __match_any_sync(am, bin);
+    if ((threadIdx.x & 31) == (__ffs(peers) - 1)) atomicAdd(&hb[bin], __popc(peers));
+}
+
+__global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackThreads)
+    prefill_pack_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t hist[2][256];
@@ -69,7 +120,6 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPrefi
     __shared__ int scan_sm[33];
     __shared__ int xchg[2];
     __shared__ int bc[8];
-    __shared__ unsigned long long prefix_sh;
 
     if (ctl->abort) return;  // uniform for the whole grid
     const int CL = kPrefillCluster;
@@ -95,30 +145,12 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPrefi
     const uint8_t* vbase = a.v + row0;
 
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
-    const int keys_bytes = ((a.chunk_cap * 8) + 15) & ~15;
-    uint8_t* stage_all = smem + keys_bytes;
-    int32_t* list = reinterpret_cast<int32_t*>(stage_all);  // reused after phase 1
+    int32_t* list = reinterpret_cast<int32_t*>(smem + (size_t)a.chunk_cap * 8);
 
-    // ---------------------------------------------------------------- 1. score
+    // ---------------------------------------------------------------- 1. keys -> smem
     {
-        const int n_sets = (n + 15) / 16;
-        const int my_sets = n_sets > wid ? (n_sets - wid + nw - 1) / nw : 0;
-        uint8_t* stage = stage_all + wid * (kPrefillStages * kStageBytes);
-        warp_stream_sumsq<kPrefillStages>(
-            my_sets, s.row_bytes, s.w, s.dtype, stage,
-            [&](int set, int row) -> const uint8_t* {
-                const int tok = lo + (wid + set * nw) * 16 + (row & 15);
-                if (tok >= hi) return nullptr;
-                return (row < 16 ? kbase : vbase) + (int64_t)tok * a.token_stride;
-            },
-            [&](int set, double sq, bool present) {
-                const double v2 = __shfl_down_sync(0xFFFFFFFFu, sq, 16);
-                if (lane < 16 && present) {
-                    const int tok = lo + (wid + set * nw) * 16 + lane;
-                    keys[tok - lo] =
-                        static_cast<unsigned long long>(__double_as_longlong(token_score_from_sumsq(sq, v2)));
-                }
-            });
+        const unsigned long long* g = a.keys + a.tab_keybase[i] + lo;
+        for (int j = tid; j < n; j += nthr) keys[j] = __ldcs(g + j);
     }
     __syncthreads();
 
@@ -134,10 +166,11 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPrefi
             uint32_t* hb = hist[pass & 1];
             for (int b = tid; b < 256; b += nthr) hb[b] = 0;
             __syncthreads();
-            for (int j = tid; j < n; j += nthr) {
-                const unsigned long long key = keys[j];
-                const bool match = (pass == 0) || ((key >> (shift + 8)) == prefix);
-                if (match) atomicAdd(&hb[(key >> shift) & 255u], 1u);
+            const int n_round = (n + nthr - 1) / nthr * nthr;
+            for (int j = tid; j < n_round; j += nthr) {
+                const unsigned long long key = j < n ? keys[j] : 0ull;
+                const bool match = j < n && ((pass == 0) || ((key >> (shift + 8)) == prefix));
+                hist_add(hb, static_cast<uint32_t>((key >> shift) & 255u), match);
             }
             cluster.sync();
             for (int b = tid; b < 256; b += nthr) {
@@ -175,7 +208,6 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPrefi
             if (done) break;
         }
     }
-    (void)prefix_sh;
 
     // ---------------------------------------------------------------- 3. compact
     auto classify = [&](unsigned long long key, bool& less, bool& tie) {

@@ -1,0 +1,252 @@
+// Exact fp64 token scores, S = ||V|| / max(||K||, 1e-12), bit-identical to
+// the reference (l2_norm: double sum of x*x in index order, kv_vector.hpp:15-21;
+// token_importance, importance.cpp:11-13).
+//
+// Register-direct, two lanes per token: lane pair (2r, 2r+1) scores token r
+// of a 16-token group. Lane q of the pair loads the 16-byte pieces q, q+2,
+// q+4, ... of the token's K row and of its V row with coalesced 128-bit
+// loads (every warp load instruction touches 16 rows x 32 contiguous bytes:
+// full-sector efficiency, no shared memory).
+//
+// bf16 — exactness certificate instead of a serial chain. Each element is
+// turned into a double by integer ops, pre-scaled by 2^-384 (bits: the bf16
+// exponent+mantissa shifted into the double's high word, exponent bias
+// +512), so x^2 is scaled by the exact power of two 2^-768. A square of a
+// bf16 value has at most 16 significant bits and its lowest set bit is at
+// or above 2*e_min - 1036 (e_min: smallest exponent field in the row, in
+// the scaled domain). If the computed sum S_c of all squares satisfies
+// S_c < 2^(2*e_min - 984) = 2^(lowest_bit + 52), then every partial sum in
+// ANY order is an exactly representable multiple of 2^lowest_bit (proof in
+// DESIGN.md §4), so the reference's sequential double sum equals the exact
+// sum equals S_c: the lanes may use several independent DFMA chains and a
+// shuffle reduction. Rows that fail the certificate (tiny or zero elements
+// relative to the row's norm; ~0.3% of N(0,1) rows) take the plain
+// sequential loop of the reference.
+//
+// fp32 — a square has up to 48 significant bits, so the certificate never
+// holds for general data: lane 0 of the pair sums the K row and lane 1 the
+// V row sequentially in index order (exact by construction).
+#pragma once
+
+#include "pe_internal.cuh"
+
+namespace pe {
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void stg_v4(void* p, uint4 v) {
+    *reinterpret_cast<uint4*>(p) = v;
+}
+
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t m, uint32_t o) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "r"(m), "r"(o));  // (a & m) | o
+    return r;
+}
+
+__device__ __forceinline__ uint32_t min3_u32(uint32_t a, uint32_t b, uint32_t c) {
+    return min(a, min(b, c));
+}
+
+// Two scaled doubles from one bf16x2 word; hmin tracks the smallest high word.
+__device__ __forceinline__ void bf16x2_scaled(uint32_t w, double& d0, double& d1, uint32_t& hmin) {
+    const uint32_t h0 = lop3_and_or(w << 13, 0x0FFFE000u, 0x20000000u);
+    const uint32_t h1 = lop3_and_or(w >> 3, 0x0FFFE000u, 0x20000000u);
+    hmin = min3_u32(hmin, h0, h1);
+    d0 = __hiloint2double(static_cast<int>(h0), 0);
+    d1 = __hiloint2double(static_cast<int>(h1), 0);
+}
+
+// Certificate check in the scaled domain (see the file comment). hmin is the
+// smallest scaled high word: exponent field = bf16 exponent + 512.
+__device__ __forceinline__ bool bf16_sum_certified(double s_scaled, uint32_t hmin) {
+    const int e_field = static_cast<int>(hmin >> 20);  // bf16 exponent + 512
+    if (e_field < 512 + 8) return false;               // zeros / subnormal-range squares
+    const int thr_field = 2 * (e_field - 512) + 39;    // 2*e_min - 984 + 1023
+    const double thr = __hiloint2double(thr_field << 20, 0);
+    return s_scaled < thr;
+}
+
+static __device__ __noinline__ double row_sumsq_seq_bf16(const uint8_t* row, int w) {
+    const uint16_t* p = reinterpret_cast<const uint16_t*>(row);
+    double acc = 0.0;
+    for (int i = 0; i < w; ++i) {
+        const double x = static_cast<double>(__uint_as_float(static_cast<uint32_t>(__ldg(p + i)) << 16));
+        acc = fma(x, x, acc);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ double row_sumsq_seq_f32(const uint8_t* row, int w) {
+    const float* p = reinterpret_cast<const float*>(row);
+    double acc = 0.0;
+    for (int i = 0; i < w; ++i) {
+        const double x = static_cast<double>(__ldg(p + i));
+        acc = fma(x, x, acc);
+    }
+    return acc;
+}
+
+// This lane's share (pieces q, q+2, ...) of one bf16 row, already loaded:
+// two DFMA chains + min tracking.
+template <int NP>
+__device__ __forceinline__ double pair_part_bf16(const uint4 (&x)[NP], uint32_t& hmin) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const uint32_t wds[4] = {x[p].x, x[p].y, x[p].z, x[p].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            double d0, d1;
+            bf16x2_scaled(wds[k], d0, d1, hmin);
+            a0 = fma(d0, d0, a0);
+            a1 = fma(d1, d1, a1);
+        }
+    }
+    return a0 + a1;
+}
+
+// Scores token `r = lane >> 1` given its K and V row pointers (both lanes of
+// the pair pass the same pointers; `valid` false -> returns 0). When kdst /
+// vdst are given, the rows are also copied there from the same registers
+// (decode append: one read of the new token serves the copy and the score).
+// PIECES = row_bytes / 16 (even).
+template <int PIECES>
+__device__ __forceinline__ double pair_token_score_bf16(const uint8_t* krow, const uint8_t* vrow, bool valid,
+                                                        uint8_t* kdst = nullptr, uint8_t* vdst = nullptr) {
+    static_assert(PIECES % 2 == 0, "even piece count");
+    constexpr int NP = PIECES / 2;
+    constexpr int W = PIECES * 8;
+    const int q = threadIdx.x & 1;
+    // K row then V row through the same registers (keeps ~32 data registers
+    // live; the warps of the SM provide the memory-level parallelism)
+    uint32_t kmin = 0xFFFFFFFFu, vmin = 0xFFFFFFFFu;
+    double kp = 0.0, vp = 0.0;
+#pragma unroll
+    for (int rv = 0; rv < 2; ++rv) {
+        const uint8_t* row = rv ? vrow : krow;
+        uint8_t* dst = rv ? vdst : kdst;
+        uint4 x[NP];
+        if (valid) {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) x[p] = ldg_stream(row + (2 * p + q) * 16);
+            if (dst != nullptr) {
+#pragma unroll
+                for (int p = 0; p < NP; ++p) stg_v4(dst + (2 * p + q) * 16, x[p]);
+            }
+        } else {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) x[p] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+        }
+        if (rv == 0) kp = pair_part_bf16<NP>(x, kmin);
+        else vp = pair_part_bf16<NP>(x, vmin);
+    }
+    kp += __shfl_xor_sync(0xFFFFFFFFu, kp, 1);
+    vp += __shfl_xor_sync(0xFFFFFFFFu, vp, 1);
+    kmin = min(kmin, __shfl_xor_sync(0xFFFFFFFFu, kmin, 1));
+    vmin = min(vmin, __shfl_xor_sync(0xFFFFFFFFu, vmin, 1));
+    if (!valid) return 0.0;
+    const double s768 = two_pow_768();
+    double k2 = kp * s768;
+    double v2 = vp * s768;
+    if (!bf16_sum_certified(kp, kmin)) k2 = row_sumsq_seq_bf16(krow, W);
+    if (!bf16_sum_certified(vp, vmin)) v2 = row_sumsq_seq_bf16(vrow, W);
+    return token_score_from_sumsq(k2, v2);
+}
+
+// fp32: lane 0 of the pair sums the K row, lane 1 the V row, sequentially
+// (and copies its row when a destination is given).
+template <int PIECES>
+__device__ __forceinline__ double pair_token_score_f32(const uint8_t* krow, const uint8_t* vrow, bool valid,
+                                                       uint8_t* kdst = nullptr, uint8_t* vdst = nullptr) {
+    const int q = threadIdx.x & 1;
+    double acc = 0.0;
+    if (valid) {
+        const uint8_t* row = q ? vrow : krow;
+        uint8_t* dst = q ? vdst : kdst;
+#pragma unroll 4
+        for (int p = 0; p < PIECES; ++p) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(row) + p);
+            if (dst != nullptr) reinterpret_cast<float4*>(dst)[p] = f;
+            double x = static_cast<double>(f.x);
+            acc = fma(x, x, acc);
+            x = static_cast<double>(f.y);
+            acc = fma(x, x, acc);
+            x = static_cast<double>(f.z);
+            acc = fma(x, x, acc);
+            x = static_cast<double>(f.w);
+            acc = fma(x, x, acc);
+        }
+    }
+    const double other = __shfl_xor_sync(0xFFFFFFFFu, acc, 1);
+    if (!valid) return 0.0;
+    const double k2 = q ? other : acc;
+    const double v2 = q ? acc : other;
+    return token_score_from_sumsq(k2, v2);
+}
+
+// Runtime-width fallbacks (rows of any multiple of 16 bytes).
+__device__ __forceinline__ double pair_token_score_generic(const uint8_t* krow, const uint8_t* vrow, bool valid,
+                                                           int w, int dtype, uint8_t* kdst = nullptr,
+                                                           uint8_t* vdst = nullptr) {
+    const int q = threadIdx.x & 1;
+    double acc = 0.0;
+    if (valid) {
+        const uint8_t* row = q ? vrow : krow;
+        uint8_t* dst = q ? vdst : kdst;
+        const int bytes = w * (dtype == PE_DTYPE_BF16 ? 2 : 4);
+        if (dst != nullptr) {
+            for (int off = 0; off < bytes; off += 16)
+                *reinterpret_cast<uint4*>(dst + off) = __ldg(reinterpret_cast<const uint4*>(row + off));
+        }
+        acc = dtype == PE_DTYPE_BF16 ? row_sumsq_seq_bf16(row, w) : row_sumsq_seq_f32(row, w);
+    }
+    const double other = __shfl_xor_sync(0xFFFFFFFFu, acc, 1);
+    if (!valid) return 0.0;
+    return token_score_from_sumsq(q ? other : acc, q ? acc : other);
+}
+
+// Row geometry the kernels are specialised for: (dtype, 16-byte pieces/row).
+enum ScoreVariant : int {
+    kScoreGeneric = 0,
+    kScoreBf16x16 = 1,  // bf16, d = 128  (256-byte rows)
+    kScoreBf16x8 = 2,   // bf16, d = 64
+    kScoreF32x16 = 3,   // fp32, d = 64   (256-byte rows)
+    kScoreF32x32 = 4,   // fp32, d = 128
+};
+
+__host__ __device__ inline int score_variant(int dtype, int row_bytes) {
+    if (dtype == PE_DTYPE_BF16 && row_bytes == 256) return kScoreBf16x16;
+    if (dtype == PE_DTYPE_BF16 && row_bytes == 128) return kScoreBf16x8;
+    if (dtype == PE_DTYPE_F32 && row_bytes == 256) return kScoreF32x16;
+    if (dtype == PE_DTYPE_F32 && row_bytes == 512) return kScoreF32x32;
+    return kScoreGeneric;
+}
+
+template <int V>
+__device__ __forceinline__ double pair_token_score(const uint8_t* krow, const uint8_t* vrow, bool valid, int w,
+                                                   int dtype, uint8_t* kdst = nullptr, uint8_t* vdst = nullptr) {
+    if constexpr (V == kScoreBf16x16) return pair_token_score_bf16<16>(krow, vrow, valid, kdst, vdst);
+    else if constexpr (V == kScoreBf16x8) return pair_token_score_bf16<8>(krow, vrow, valid, kdst, vdst);
+    else if constexpr (V == kScoreF32x16) return pair_token_score_f32<16>(krow, vrow, valid, kdst, vdst);
+    else if constexpr (V == kScoreF32x32) return pair_token_score_f32<32>(krow, vrow, valid, kdst, vdst);
+    else return pair_token_score_generic(krow, vrow, valid, w, dtype, kdst, vdst);
+}
+
+// Dispatch helper for kernel templates.
+#define PE_SCORE_DISPATCH(variant, KERNEL_CALL)            \
+    switch (variant) {                                     \
+    case kScoreBf16x16: { constexpr int SV = kScoreBf16x16; KERNEL_CALL; } break; \
+    case kScoreBf16x8: { constexpr int SV = kScoreBf16x8; KERNEL_CALL; } break;   \
+    case kScoreF32x16: { constexpr int SV = kScoreF32x16; KERNEL_CALL; } break;   \
+    case kScoreF32x32: { constexpr int SV = kScoreF32x32; KERNEL_CALL; } break;   \
+    default: { constexpr int SV = kScoreGeneric; KERNEL_CALL; } break;           \
+    }
+
+}  // namespace pe

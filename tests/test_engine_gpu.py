@@ -230,10 +230,12 @@ def test_error_statuses():
     # empty prefill -> Error (policy.cpp:57-58)
     with pytest.raises(pe.Error):
         eng.prefill_compress(0, dev(k), dev(k), np.array([0, 0], np.int32), seq_begin=1)
-    # GQA shape mismatch -> LengthMismatch
-    out = torch.empty((2, 3, 8), dtype=torch.float32, device="cuda")
+    # GQA shape mismatch -> LengthMismatch (3 query heads over 2 KV heads)
+    geo = pe.EngineGeometry(n_seqs=1, n_layers=1, n_kv_heads=2, head_dim=8, dtype=oracle.F32)
+    eng2 = pe.PagedEvictionEngine(geo, pe.PolicyConfig(cache_budget=8, page_size=4))
+    out = torch.empty((1, 3, 8), dtype=torch.float32, device="cuda")
     with pytest.raises(pe.LengthMismatch):
-        eng.attend(0, dev(np.ones((2, 3, 8), np.float32)), out, 3)
+        eng2.attend(0, dev(np.ones((1, 3, 8), np.float32)), out, 3)
 
 
 @pytest.mark.slow
