@@ -15,6 +15,8 @@
 // log2e folded into the scale) and accumulates P.V with one lane per
 // d/32-dimension slice. Warp and split partials are merged with the usual
 // (max, sum) log-sum-exp rescaling.
+#include <cuda_bf16.h>
+
 #include "pe_kernels.cuh"
 
 namespace pe {
@@ -242,6 +244,236 @@ __global__ void __launch_bounds__(kAttnThreads) attention_split_kernel(DevState 
             a.part_ml[pidx * 2 + 1] = ll;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-core variant for bf16 caches with B = 16 (one MMA k-step per page).
+// Per warp and page: the page (16 K rows + 16 V rows) is staged into padded
+// shared memory with cp.async (3-stage ring), then
+//   S = Q K^T   mma.sync m16n8k16: M = query heads of the KV head (G <= 8,
+//               zero-padded to 16), N = 8 tokens, K = 16 dims (ldmatrix);
+//   online softmax on the S fragments in fp32 (exp2, log2e folded into the
+//               scale; slots past the newest page's fill masked to -inf);
+//   O += P V    M = heads, N = 8 dims, K = 16 tokens (ldmatrix.trans), with
+//               P split into bf16 hi + lo halves (two MMAs) so the bf16
+//               rounding of the weights stays ~2^-17 relative.
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void split_bf16x2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    hi = pack_bf16x2(x0, x1);
+    const float h0 = __uint_as_float(hi << 16);
+    const float h1 = __uint_as_float(hi & 0xFFFF0000u);
+    lo = pack_bf16x2(x0 - h0, x1 - h1);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kAttnThreads, 2) attention_mma_kernel(DevState s, AttnArgs a) {
+    constexpr int RB = D * 2;          // bf16 row bytes
+    constexpr int RP = RB + 16;        // padded smem row pitch (conflict-free ldmatrix)
+    constexpr int PAGE_SM = 32 * RP;   // 16 K rows + 16 V rows
+    constexpr int NST = 3;             // cp.async stages per warp
+    constexpr int KS = D / 16;         // QK k-steps
+    constexpr int NT = D / 8;          // PV n-tiles
+    constexpr int PIECES = RB / 16;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    const int i = blockIdx.y;
+    const int sp = blockIdx.x;
+    const int H = s.tab_heads;
+    const int h = i % H;
+    const int seq = i / H;
+    const int t = (seq * s.n_layers + a.layer) * H + h;
+    const int G = a.G;
+    const int N = s.num_pages[t];
+    const int p_begin = sp * a.pages_per_split;
+    const int p_end = min(N, p_begin + a.pages_per_split);
+    const int g = lane >> 2;
+    const int tq = lane & 3;
+
+    uint8_t* stage = smem + wid * NST * PAGE_SM;
+    float* wpart_o = reinterpret_cast<float*>(smem + nw * NST * PAGE_SM);  // [nw][G][D]
+    float* wpart_ml = wpart_o + nw * G * D;                                 // [nw][G][2]
+
+    // Q fragments (A operand, rows g < G real)
+    uint32_t qa[KS][2];
+    {
+        const uint8_t* qrow = a.q + ((int64_t)seq * a.n_q_heads + h * G + min(g, G - 1)) * RB;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            qa[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + (16 * ks + 2 * tq) * 2) : 0u;
+            qa[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + (16 * ks + 2 * tq + 8) * 2) : 0u;
+        }
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+    float m = -INFINITY, l = 0.f;
+
+    const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
+    const int my_n = (p_end - p_begin) > wid ? ((p_end - p_begin) - wid + nw - 1) / nw : 0;
+    auto issue = [&](int k) {
+        if (k < my_n) {
+            const int pg = p_begin + wid + k * nw;
+            const uint8_t* base = s.pages + (int64_t)__ldg(row + pg) * 32 * RB;
+            uint8_t* st = stage + (k % NST) * PAGE_SM;
+#pragma unroll
+            for (int x = lane; x < 32 * PIECES; x += 32) {
+                const int r = x / PIECES;
+                const int pc = x - r * PIECES;
+                cp_async16(st + r * RP + pc * 16, base + r * RB + pc * 16);
+            }
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < NST - 1; ++k) issue(k);
+
+    const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+    const int lm_j = lane >> 3, lm_r = lane & 7;
+    for (int k = 0; k < my_n; ++k) {
+        issue(k + NST - 1);
+        cp_async_wait<NST - 1>();
+        __syncwarp();
+        const int pg = p_begin + wid + k * nw;
+        const int fill = (pg == N - 1) ? s.newest_fill[t] : 16;
+        const uint32_t st = stage_s + (k % NST) * PAGE_SM;
+        // ---- S = Q K^T (two n-tiles of 8 tokens)
+        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            uint32_t b0, b1, b2, b3;
+            const int tok = (lm_j >> 1) * 8 + lm_r;
+            const int dcol = 16 * ks + (lm_j & 1) * 8;
+            ldsm_x4(st + tok * RP + dcol * 2, b0, b1, b2, b3);
+            mma_bf16_16816(sc[0], qa[ks][0], qa[ks][1], b0, b1);
+            mma_bf16_16816(sc[1], qa[ks][0], qa[ks][1], b2, b3);
+        }
+        // ---- online softmax on row g (columns: tokens 8nt + 2tq, +1)
+        float x[2][2];
+        float rmax = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int tok = 8 * nt + 2 * tq + j;
+                x[nt][j] = tok < fill ? sc[nt][j] * a.scale_log2 : -INFINITY;
+                rmax = fmaxf(rmax, x[nt][j]);
+            }
+        }
+        rmax = fmaxf(rmax, __shfl_xor_sync(0xFFFFFFFFu, rmax, 1));
+        rmax = fmaxf(rmax, __shfl_xor_sync(0xFFFFFFFFu, rmax, 2));
+        const float m_new = fmaxf(m, rmax);
+        const float corr = exp2f(m - m_new);
+        float rsum = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                x[nt][j] = exp2f(x[nt][j] - m_new);
+                rsum += x[nt][j];
+            }
+        }
+        rsum += __shfl_xor_sync(0xFFFFFFFFu, rsum, 1);
+        rsum += __shfl_xor_sync(0xFFFFFFFFu, rsum, 2);
+        l = l * corr + rsum;
+        m = m_new;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            o[nt][0] *= corr;
+            o[nt][1] *= corr;
+        }
+        // ---- O += P V (P = hi + lo bf16 halves)
+        uint32_t ph0, pl0, ph1, pl1;
+        split_bf16x2(x[0][0], x[0][1], ph0, pl0);
+        split_bf16x2(x[1][0], x[1][1], ph1, pl1);
+#pragma unroll
+        for (int ntp = 0; ntp < NT / 2; ++ntp) {
+            uint32_t b0, b1, b2, b3;
+            const int tok = (lm_j & 1) * 8 + lm_r;
+            const int dd = 16 * ntp + (lm_j >> 1) * 8;
+            ldsm_x4_t(st + (16 + tok) * RP + dd * 2, b0, b1, b2, b3);
+            mma_bf16_16816(o[2 * ntp], ph0, ph1, b0, b1);
+            mma_bf16_16816(o[2 * ntp], pl0, pl1, b0, b1);
+            mma_bf16_16816(o[2 * ntp + 1], ph0, ph1, b2, b3);
+            mma_bf16_16816(o[2 * ntp + 1], pl0, pl1, b2, b3);
+        }
+        __syncwarp();
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // stage memory is reused for the partials below? (separate region) keep warps aligned
+
+    // ---- warp partials -> smem (row g < G: dims 8nt + 2tq, +1)
+    if (g < G) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            wpart_o[(wid * G + g) * D + 8 * nt + 2 * tq] = o[nt][0];
+            wpart_o[(wid * G + g) * D + 8 * nt + 2 * tq + 1] = o[nt][1];
+        }
+        if (tq == 0) {
+            wpart_ml[(wid * G + g) * 2] = m;
+            wpart_ml[(wid * G + g) * 2 + 1] = l;
+        }
+    }
+    __syncthreads();
+    const int n_splits = a.splits;
+    for (int xi = threadIdx.x; xi < G * D; xi += blockDim.x) {
+        const int gg = xi / D;
+        float mm = -INFINITY;
+        for (int w2 = 0; w2 < nw; ++w2) mm = fmaxf(mm, wpart_ml[(w2 * G + gg) * 2]);
+        float ll = 0.f, oo = 0.f;
+        for (int w2 = 0; w2 < nw; ++w2) {
+            const float mw = wpart_ml[(w2 * G + gg) * 2];
+            const float c = (mw == -INFINITY) ? 0.f : exp2f(mw - mm);
+            ll += wpart_ml[(w2 * G + gg) * 2 + 1] * c;
+            oo += wpart_o[(w2 * G + gg) * D + (xi % D)] * c;
+        }
+        const int64_t pidx = ((int64_t)i * n_splits + sp) * G + gg;
+        a.part_o[pidx * D + (xi % D)] = oo;
+        if (xi % D == 0) {
+            a.part_ml[pidx * 2] = mm;
+            a.part_ml[pidx * 2 + 1] = ll;
+        }
+    }
+}
+
+size_t attention_mma_smem(int d, int G) {
+    const int nw = kAttnThreads / 32;
+    return (size_t)nw * 3 * 32 * (2 * d + 16) + (size_t)nw * G * d * 4 + (size_t)nw * G * 2 * 4;
+}
+
+void launch_attention_mma(int d, dim3 grid, size_t smem, cudaStream_t st, const DevState& s, const AttnArgs& a) {
+    if (d == 128) attention_mma_kernel<128><<<grid, kAttnThreads, smem, st>>>(s, a);
+    else attention_mma_kernel<64><<<grid, kAttnThreads, smem, st>>>(s, a);
+}
+
+const void* attention_mma_fn(int d) {
+    return d == 128 ? reinterpret_cast<const void*>(attention_mma_kernel<128>)
+                    : reinterpret_cast<const void*>(attention_mma_kernel<64>);
 }
 
 // merge the split partials: out = sum_s o_s * 2^(m_s - M) / sum_s l_s * 2^(m_s - M)

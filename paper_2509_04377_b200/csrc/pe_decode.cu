@@ -207,7 +207,7 @@ __device__ __forceinline__ void finalize_evict(const DevState& s, int t, int i, 
 // slot-order sum / fill (score_pages -> page_score, importance.cpp:19-39).
 // The last CTA of the table (atomic ticket) takes the argmin and evicts.
 template <int SV>
-__global__ void __launch_bounds__(kEvictThreads, 3) evict_score_kernel(
+__global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
     DevState s, TableSet ts, int pages_per_cta, const int32_t* __restrict__ work,
     const int32_t* __restrict__ rank, const LaunchCtl* __restrict__ ctl, double* scratch,
     int32_t* tickets, int32_t* victims) {
@@ -229,19 +229,34 @@ __global__ void __launch_bounds__(kEvictThreads, 3) evict_score_kernel(
     const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
     const int64_t page_bytes = (int64_t)2 * s.B * s.pitch;
 
-    for (int lp = wid; lp < np; lp += nw) {
-        const int id = __ldg(row + p0 + lp);
-        const uint8_t* base = s.pages + (int64_t)id * page_bytes;
-        double sum = 0.0;
-        for (int s0 = 0; s0 < s.B; s0 += 16) {
-            const int slot = s0 + (lane >> 1);
-            const bool valid = slot < s.B;
-            const double S = pair_token_score<SV>(base + (int64_t)slot * s.pitch,
-                                                  base + (int64_t)(s.B + slot) * s.pitch, valid, s.w, s.dtype);
-            const int ns = min(16, s.B - s0);
-            for (int j = 0; j < ns; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+    if (s.B == 16) {
+        // one 16-slot group per page, read straight into registers (no
+        // prefetch buffer: occupancy, i.e. warps in flight, hides HBM latency)
+        const int slot = lane >> 1;
+        const int64_t ko = (int64_t)slot * s.pitch, vo = (int64_t)(16 + slot) * s.pitch;
+        for (int lp = wid; lp < np; lp += nw) {
+            const uint8_t* base = s.pages + (int64_t)__ldg(row + p0 + lp) * page_bytes;
+            const double S = pair_token_score<SV>(base + ko, base + vo, true, s.w, s.dtype);
+            double sum = 0.0;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+            if (lane == 0) page_mean[lp] = sum / 16.0;
         }
-        if (lane == 0) page_mean[lp] = sum / static_cast<double>(s.B);
+    } else {
+        for (int lp = wid; lp < np; lp += nw) {
+            const int id = __ldg(row + p0 + lp);
+            const uint8_t* base = s.pages + (int64_t)id * page_bytes;
+            double sum = 0.0;
+            for (int s0 = 0; s0 < s.B; s0 += 16) {
+                const int slot = s0 + (lane >> 1);
+                const bool valid = slot < s.B;
+                const double S = pair_token_score<SV>(base + (int64_t)slot * s.pitch,
+                                                      base + (int64_t)(s.B + slot) * s.pitch, valid, s.w, s.dtype);
+                const int ns = min(16, s.B - s0);
+                for (int j = 0; j < ns; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+            }
+            if (lane == 0) page_mean[lp] = sum / static_cast<double>(s.B);
+        }
     }
     __syncthreads();
     for (int j = threadIdx.x; j < np; j += blockDim.x) {

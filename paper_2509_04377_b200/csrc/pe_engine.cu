@@ -304,8 +304,10 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             *out = optin - static_cast<int>(fa.sharedSizeBytes);
             return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, *out) == cudaSuccess;
         };
+        int mma64 = 0, mma128 = 0;
         if (!allow(reinterpret_cast<const void*>(prefill_pack_kernel), &e->max_dyn_prefill) ||
-            !allow(reinterpret_cast<const void*>(attention_split_kernel), &e->max_dyn_attn)) {
+            !allow(reinterpret_cast<const void*>(attention_split_kernel), &e->max_dyn_attn) ||
+            !allow(attention_mma_fn(64), &mma64) || !allow(attention_mma_fn(128), &mma128)) {
             cudaGetLastError();
             return cleanup_fail(fail(PE_CUDA_ERROR, "cudaFuncSetAttribute(max dynamic smem) failed"));
         }
@@ -407,7 +409,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     a.chunk_cap = chunk_cap;
     if (total_pages > INT32_MAX) return fail(PE_POOL_EXHAUSTED, "page pool exhausted");
     plan_prefill_kernel<<<1, 1024, 0, st>>>(s, a, static_cast<int32_t>(total_pages), e->ctl);
-    launch_prefill_score_any(e->variant, dim3((max_len + kScoreTokensPerCta - 1) / kScoreTokensPerCta, n_tab), st, s,
+    launch_prefill_score_any(e->variant, dim3((max_len + kScoreTokensPerCta - 1) / kScoreTokensPerCta, n_seqs), st, s,
                              a, e->ctl);
     prefill_pack_kernel<<<dim3(kPrefillCluster, n_tab), kPackThreads, pack_smem, st>>>(s, a, e->ctl);
     r = check_launch(e, "prefill_kernel");
@@ -539,11 +541,18 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
     a.splits = splits;
     a.pages_per_split = pps;
     a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(s.w)));
-    const int nw = 4;
-    size_t smem = (size_t)G * s.w * 4 + (size_t)nw * G * 16 * 4 + (size_t)nw * G * s.w * 4 +
-                  (size_t)nw * G * 2 * 4 + 16 + (size_t)nw * 2 * (2 * s.B * (s.row_bytes + 16));
-    if (smem > (size_t)e->max_dyn_attn) return fail(PE_INVALID_ARG, "attention tile exceeds shared memory");
-    attention_split_kernel<<<dim3(splits, n_tab), 128, smem, st>>>(s, a);
+    const bool use_mma = s.dtype == PE_DTYPE_BF16 && s.B == 16 && (s.w == 64 || s.w == 128);
+    if (use_mma) {
+        // tensor-core path (mma.sync bf16, P split hi/lo), pe_attention.cu
+        const size_t smem = attention_mma_smem(s.w, G);
+        launch_attention_mma(s.w, dim3(splits, n_tab), smem, st, s, a);
+    } else {
+        const int nw = 4;
+        size_t smem = (size_t)G * s.w * 4 + (size_t)nw * G * 16 * 4 + (size_t)nw * G * s.w * 4 +
+                      (size_t)nw * G * 2 * 4 + 16 + (size_t)nw * 2 * (2 * s.B * (s.row_bytes + 16));
+        if (smem > (size_t)e->max_dyn_attn) return fail(PE_INVALID_ARG, "attention tile exceeds shared memory");
+        attention_split_kernel<<<dim3(splits, n_tab), 128, smem, st>>>(s, a);
+    }
     attention_merge_kernel<<<n_tab, 128, 0, st>>>(s, a);
     r = check_launch(e, "attention");
     if (r != PE_OK) return r;

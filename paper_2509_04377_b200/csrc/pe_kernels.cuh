@@ -13,7 +13,7 @@ constexpr int kAppendThreads = 128;      // 4 warps x 16 tables
 constexpr int kEvictThreads = 128;       // 4 warps per CTA
 constexpr int kMaxPagesPerCta = 64;
 constexpr int kPrefillThreads = 128;     // score kernel: 4 warps per CTA
-constexpr int kScoreTokensPerCta = 512;  // 4 warps x 8 groups x 16 tokens
+constexpr int kScoreTokensPerCta = 256;  // tokens (x all heads) per score CTA
 constexpr int kPackThreads = 256;        // select/pack kernel: 8 warps per CTA
 constexpr int kPrefillCluster = 8;       // CTAs per table (portable cluster size)
 
@@ -59,6 +59,10 @@ struct AttnArgs {
     float scale_log2;        // log2(e)/sqrt(d)
 };
 __global__ void attention_split_kernel(DevState s, AttnArgs a);
+// tensor-core variant (bf16, B = 16, d in {64, 128}, G <= 8)
+size_t attention_mma_smem(int d, int G);
+void launch_attention_mma(int d, dim3 grid, size_t smem, cudaStream_t st, const DevState& s, const AttnArgs& a);
+const void* attention_mma_fn(int d);
 __global__ void attention_merge_kernel(DevState s, AttnArgs a);
 
 }  // namespace pe

@@ -64,31 +64,39 @@ __global__ void __launch_bounds__(1024) plan_prefill_kernel(DevState s, PrefillA
 }
 
 // ---------------------------------------------------------------------------
-// prefill_score_kernel: grid (ceil(maxL / 512), n_tab), 4 warps; each warp
-// scores 8 groups of 16 tokens (lane pair per token).
+// prefill_score_kernel: grid (ceil(maxL / 256), n_seqs of the launch), 4
+// warps. The CTA scores tokens [256*bx, 256*bx+256) of one sequence for ALL
+// its tables (heads): the input is token-major [tokens][heads][w], so the
+// (token, head) rows of a token block are one contiguous span and every
+// warp step (16 lane pairs = 16 consecutive (token, head) rows of K and of
+// V) reads 4 KB of contiguous HBM.
 template <int SV>
 __global__ void __launch_bounds__(kPrefillThreads) prefill_score_kernel(DevState s, PrefillArgs a,
                                                                          const LaunchCtl* ctl) {
     if (ctl->abort) return;
-    const int i = blockIdx.y;
-    const int L = a.tab_len[i];
+    const int sq = blockIdx.y;  // sequence within the launch
+    const int H = s.tab_heads;
+    const int L = a.tab_len[sq * H];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    const int tok_cta = blockIdx.x * kScoreTokensPerCta;
-    if (tok_cta >= L) return;
-    const int h = i % s.tab_heads;
-    const int64_t row0 = (a.tab_tok0[i] * s.tab_heads + h) * (int64_t)s.row_bytes;
-    const uint8_t* kbase = a.k + row0;
-    const uint8_t* vbase = a.v + row0;
-    unsigned long long* keys = a.keys + a.tab_keybase[i];
-    constexpr int kGroups = kScoreTokensPerCta / 16 / (kPrefillThreads / 32);
-#pragma unroll 1
-    for (int g = 0; g < kGroups; ++g) {
-        const int tok = tok_cta + (wid * kGroups + g) * 16 + (lane >> 1);
-        const bool valid = tok < L;
-        const double S = pair_token_score<SV>(kbase + (int64_t)tok * a.token_stride,
-                                              vbase + (int64_t)tok * a.token_stride, valid, s.w, s.dtype);
-        if (valid && (lane & 1) == 0) keys[tok] = static_cast<unsigned long long>(__double_as_longlong(S));
+    const int nw = blockDim.x >> 5;
+    const int tok_lo = blockIdx.x * kScoreTokensPerCta;
+    if (tok_lo >= L) return;
+    const int tok_hi = min(L, tok_lo + kScoreTokensPerCta);
+    const int64_t f_lo = (int64_t)tok_lo * H;
+    const int64_t f_hi = (int64_t)tok_hi * H;
+    const int64_t row0 = a.tab_tok0[sq * H] * H;  // first (token, head) row of the sequence
+    const int64_t n_units = (f_hi - f_lo + 15) / 16;
+    for (int64_t u = wid; u < n_units; u += nw) {
+        const int64_t f = f_lo + u * 16 + (lane >> 1);
+        const bool valid = f < f_hi;
+        const int64_t off = (row0 + f) * s.row_bytes;
+        const double S = pair_token_score<SV>(a.k + off, a.v + off, valid, s.w, s.dtype);
+        if (valid && (lane & 1) == 0) {
+            const int tok = static_cast<int>(f / H);
+            const int h = static_cast<int>(f - (int64_t)tok * H);
+            a.keys[a.tab_keybase[sq * H + h] + tok] = static_cast<unsigned long long>(__double_as_longlong(S));
+        }
     }
 }
 

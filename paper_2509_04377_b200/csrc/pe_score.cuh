@@ -3,10 +3,10 @@
 // token_importance, importance.cpp:11-13).
 //
 // Register-direct, two lanes per token: lane pair (2r, 2r+1) scores token r
-// of a 16-token group. Lane q of the pair loads the 16-byte pieces q, q+2,
-// q+4, ... of the token's K row and of its V row with coalesced 128-bit
-// loads (every warp load instruction touches 16 rows x 32 contiguous bytes:
-// full-sector efficiency, no shared memory).
+// of a 16-token group. Lane q of the pair loads the 32-byte chunks q, q+2,
+// ... of the token's K row and of its V row with 256-bit loads (one full
+// sector per lane; every warp load instruction touches 16 rows x 64
+// contiguous bytes; no shared memory).
 //
 // bf16 — exactness certificate instead of a serial chain. Each element is
 // turned into a double by integer ops, pre-scaled by 2^-384 (bits: the bf16
@@ -42,6 +42,25 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
 
 __device__ __forceinline__ void stg_v4(void* p, uint4 v) {
     *reinterpret_cast<uint4*>(p) = v;
+}
+
+// 256-bit streaming load (one full 32-byte sector per lane; LDG.E.256 on
+// sm_100a) with an L2 prefetch of the enclosing 256-byte segment.
+struct u32x8 {
+    uint32_t w[8];
+};
+__device__ __forceinline__ u32x8 ldg256(const void* p) {
+    u32x8 r;
+    asm("ld.global.nc.L1::no_allocate.L2::256B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]),
+          "=r"(r.w[7])
+        : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void stg256(void* p, const u32x8& v) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]),
+                 "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+                 : "memory");
 }
 
 __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t m, uint32_t o) {
@@ -93,18 +112,17 @@ __device__ __forceinline__ double row_sumsq_seq_f32(const uint8_t* row, int w) {
     return acc;
 }
 
-// This lane's share (pieces q, q+2, ...) of one bf16 row, already loaded:
-// two DFMA chains + min tracking.
-template <int NP>
-__device__ __forceinline__ double pair_part_bf16(const uint4 (&x)[NP], uint32_t& hmin) {
+// This lane's share (32-byte chunks q, q+2, ...) of one bf16 row, already
+// loaded: two DFMA chains + min tracking.
+template <int NC>
+__device__ __forceinline__ double pair_part_bf16(const u32x8 (&x)[NC], uint32_t& hmin) {
     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        const uint32_t wds[4] = {x[p].x, x[p].y, x[p].z, x[p].w};
+    for (int c = 0; c < NC; ++c) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < 8; ++k) {
             double d0, d1;
-            bf16x2_scaled(wds[k], d0, d1, hmin);
+            bf16x2_scaled(x[c].w[k], d0, d1, hmin);
             a0 = fma(d0, d0, a0);
             a1 = fma(d1, d1, a1);
         }
@@ -112,40 +130,47 @@ __device__ __forceinline__ double pair_part_bf16(const uint4 (&x)[NP], uint32_t&
     return a0 + a1;
 }
 
+__device__ __forceinline__ u32x8 bf16_ones8() {
+    u32x8 r;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r.w[k] = 0x3F803F80u;
+    return r;
+}
+
 // Scores token `r = lane >> 1` given its K and V row pointers (both lanes of
-// the pair pass the same pointers; `valid` false -> returns 0). When kdst /
-// vdst are given, the rows are also copied there from the same registers
-// (decode append: one read of the new token serves the copy and the score).
-// PIECES = row_bytes / 16 (even).
-template <int PIECES>
+// the pair pass the same pointers; `valid` false -> returns 0). Lane q of the
+// pair loads the 32-byte chunks q, q+2, ... (one full sector per lane per
+// 256-bit load; a warp load covers 16 rows x 64 contiguous bytes). When
+// kdst / vdst are given the rows are also copied there from the same
+// registers (decode append: one read serves the copy and the score).
+// CHUNKS = row_bytes / 32 (even).
+template <int CHUNKS>
 __device__ __forceinline__ double pair_token_score_bf16(const uint8_t* krow, const uint8_t* vrow, bool valid,
                                                         uint8_t* kdst = nullptr, uint8_t* vdst = nullptr) {
-    static_assert(PIECES % 2 == 0, "even piece count");
-    constexpr int NP = PIECES / 2;
-    constexpr int W = PIECES * 8;
+    static_assert(CHUNKS % 2 == 0, "even chunk count");
+    constexpr int NC = CHUNKS / 2;
+    constexpr int W = CHUNKS * 16;
     const int q = threadIdx.x & 1;
-    // K row then V row through the same registers (keeps ~32 data registers
-    // live; the warps of the SM provide the memory-level parallelism)
     uint32_t kmin = 0xFFFFFFFFu, vmin = 0xFFFFFFFFu;
     double kp = 0.0, vp = 0.0;
 #pragma unroll
     for (int rv = 0; rv < 2; ++rv) {
         const uint8_t* row = rv ? vrow : krow;
         uint8_t* dst = rv ? vdst : kdst;
-        uint4 x[NP];
+        u32x8 x[NC];
         if (valid) {
 #pragma unroll
-            for (int p = 0; p < NP; ++p) x[p] = ldg_stream(row + (2 * p + q) * 16);
+            for (int c = 0; c < NC; ++c) x[c] = ldg256(row + (2 * c + q) * 32);
             if (dst != nullptr) {
 #pragma unroll
-                for (int p = 0; p < NP; ++p) stg_v4(dst + (2 * p + q) * 16, x[p]);
+                for (int c = 0; c < NC; ++c) stg256(dst + (2 * c + q) * 32, x[c]);
             }
         } else {
 #pragma unroll
-            for (int p = 0; p < NP; ++p) x[p] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+            for (int c = 0; c < NC; ++c) x[c] = bf16_ones8();
         }
-        if (rv == 0) kp = pair_part_bf16<NP>(x, kmin);
-        else vp = pair_part_bf16<NP>(x, vmin);
+        if (rv == 0) kp = pair_part_bf16<NC>(x, kmin);
+        else vp = pair_part_bf16<NC>(x, vmin);
     }
     kp += __shfl_xor_sync(0xFFFFFFFFu, kp, 1);
     vp += __shfl_xor_sync(0xFFFFFFFFu, vp, 1);
@@ -162,7 +187,7 @@ __device__ __forceinline__ double pair_token_score_bf16(const uint8_t* krow, con
 
 // fp32: lane 0 of the pair sums the K row, lane 1 the V row, sequentially
 // (and copies its row when a destination is given).
-template <int PIECES>
+template <int CHUNKS>
 __device__ __forceinline__ double pair_token_score_f32(const uint8_t* krow, const uint8_t* vrow, bool valid,
                                                        uint8_t* kdst = nullptr, uint8_t* vdst = nullptr) {
     const int q = threadIdx.x & 1;
@@ -170,18 +195,15 @@ __device__ __forceinline__ double pair_token_score_f32(const uint8_t* krow, cons
     if (valid) {
         const uint8_t* row = q ? vrow : krow;
         uint8_t* dst = q ? vdst : kdst;
-#pragma unroll 4
-        for (int p = 0; p < PIECES; ++p) {
-            const float4 f = __ldg(reinterpret_cast<const float4*>(row) + p);
-            if (dst != nullptr) reinterpret_cast<float4*>(dst)[p] = f;
-            double x = static_cast<double>(f.x);
-            acc = fma(x, x, acc);
-            x = static_cast<double>(f.y);
-            acc = fma(x, x, acc);
-            x = static_cast<double>(f.z);
-            acc = fma(x, x, acc);
-            x = static_cast<double>(f.w);
-            acc = fma(x, x, acc);
+#pragma unroll 2
+        for (int c = 0; c < CHUNKS; ++c) {
+            const u32x8 f = ldg256(row + c * 32);
+            if (dst != nullptr) stg256(dst + c * 32, f);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double x = static_cast<double>(__uint_as_float(f.w[k]));
+                acc = fma(x, x, acc);
+            }
         }
     }
     const double other = __shfl_xor_sync(0xFFFFFFFFu, acc, 1);
@@ -232,10 +254,10 @@ __host__ __device__ inline int score_variant(int dtype, int row_bytes) {
 template <int V>
 __device__ __forceinline__ double pair_token_score(const uint8_t* krow, const uint8_t* vrow, bool valid, int w,
                                                    int dtype, uint8_t* kdst = nullptr, uint8_t* vdst = nullptr) {
-    if constexpr (V == kScoreBf16x16) return pair_token_score_bf16<16>(krow, vrow, valid, kdst, vdst);
-    else if constexpr (V == kScoreBf16x8) return pair_token_score_bf16<8>(krow, vrow, valid, kdst, vdst);
-    else if constexpr (V == kScoreF32x16) return pair_token_score_f32<16>(krow, vrow, valid, kdst, vdst);
-    else if constexpr (V == kScoreF32x32) return pair_token_score_f32<32>(krow, vrow, valid, kdst, vdst);
+    if constexpr (V == kScoreBf16x16) return pair_token_score_bf16<8>(krow, vrow, valid, kdst, vdst);
+    else if constexpr (V == kScoreBf16x8) return pair_token_score_bf16<4>(krow, vrow, valid, kdst, vdst);
+    else if constexpr (V == kScoreF32x16) return pair_token_score_f32<8>(krow, vrow, valid, kdst, vdst);
+    else if constexpr (V == kScoreF32x32) return pair_token_score_f32<16>(krow, vrow, valid, kdst, vdst);
     else return pair_token_score_generic(krow, vrow, valid, w, dtype, kdst, vdst);
 }
 
