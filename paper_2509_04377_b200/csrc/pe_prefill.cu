@@ -288,38 +288,47 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackT
     __syncthreads();
 
     // ---------------------------------------------------------------- 4. pack
+    // The page ids this CTA writes (a contiguous run of the table's pages)
+    // are read once into shared memory; then lane pair r copies survivor
+    // m0 + r: K row and V row with 256-bit loads / stores (a warp moves 16
+    // survivors = 8 KB per step with 8 x 32 B requests in flight per lane).
     const int pop_base = ctl->pop_base;
     const int pagebase = a.tab_pagebase[i];
     const int B = s.B;
-    for (int m0 = wid; m0 < kept_me; m0 += nw * 4) {
-        uint4 buf[4];
-        int jj[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) jj[u] = (m0 + u * nw < kept_me) ? list[m0 + u * nw] : -1;
-        for (int off = (lane & 15) * 16; off < s.row_bytes; off += 256) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (jj[u] >= 0) {
-                    const uint8_t* src = (lane < 16 ? kbase : vbase) + (int64_t)(lo + jj[u]) * a.token_stride;
-                    buf[u] = __ldcs(reinterpret_cast<const uint4*>(src + off));
-                }
+    int32_t* page_ids = reinterpret_cast<int32_t*>(hist[0]);  // hist is free after select
+    const int pg_first = surv_base / B;
+    const int pg_count = kept_me > 0 ? (surv_base + kept_me - 1) / B - pg_first + 1 : 0;
+    for (int p = tid; p < pg_count && p < 512; p += nthr)
+        page_ids[p] = s.stack[pop_base - 1 - (pagebase + pg_first + p)];
+    __syncthreads();
+    const bool ids_cached = pg_count <= 512;
+    for (int m0 = wid * 16; m0 < kept_me; m0 += nw * 16) {
+        const int m = m0 + (lane >> 1);
+        const bool valid = m < kept_me;
+        const int jl = valid ? list[m] : 0;
+        const int q = surv_base + m;
+        const int pidx = q / B - pg_first;
+        const int page = valid ? (ids_cached ? page_ids[pidx] : s.stack[pop_base - 1 - (pagebase + q / B)]) : 0;
+        const int slot = q % B;
+        const uint8_t* ks = kbase + (int64_t)(lo + jl) * a.token_stride;
+        const uint8_t* vs = vbase + (int64_t)(lo + jl) * a.token_stride;
+        uint8_t* kd = s.pages + (((int64_t)page * 2 + 0) * B + slot) * s.pitch;
+        uint8_t* vd = s.pages + (((int64_t)page * 2 + 1) * B + slot) * s.pitch;
+        if (valid) {
+            const int qq = lane & 1;
+            if ((s.row_bytes & 63) == 0) {
+                for (int off = qq * 32; off < s.row_bytes; off += 64) stg256(kd + off, ldg256(ks + off));
+                for (int off = qq * 32; off < s.row_bytes; off += 64) stg256(vd + off, ldg256(vs + off));
+            } else {
+                for (int off = qq * 16; off < s.row_bytes; off += 32)
+                    *reinterpret_cast<uint4*>(kd + off) = __ldcs(reinterpret_cast<const uint4*>(ks + off));
+                for (int off = qq * 16; off < s.row_bytes; off += 32)
+                    *reinterpret_cast<uint4*>(vd + off) = __ldcs(reinterpret_cast<const uint4*>(vs + off));
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (jj[u] >= 0) {
-                    const int q = surv_base + m0 + u * nw;
-                    const int page = s.stack[pop_base - 1 - (pagebase + q / B)];
-                    uint8_t* dst = s.pages + (((int64_t)page * 2 + (lane >> 4)) * B + q % B) * s.pitch;
-                    *reinterpret_cast<uint4*>(dst + off) = buf[u];
-                }
+            if (qq == 0) {
+                s.positions[(int64_t)page * B + slot] = lo + jl;
+                s.token_scores[(int64_t)page * B + slot] = __longlong_as_double(static_cast<long long>(keys[jl]));
             }
-        }
-        if (lane < 4 && jj[lane] >= 0) {
-            const int u = lane;
-            const int q = surv_base + m0 + u * nw;
-            const int page = s.stack[pop_base - 1 - (pagebase + q / B)];
-            s.positions[(int64_t)page * B + q % B] = lo + jj[u];
-            s.token_scores[(int64_t)page * B + q % B] = __longlong_as_double(static_cast<long long>(keys[jj[u]]));
         }
     }
     const int n_pages = (keep + B - 1) / B;
