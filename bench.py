@@ -281,12 +281,10 @@ def run_b200(args, cfg, world, rank, local):
             dist.barrier()
         torch.cuda.synchronize()
 
+    from paper_2509_04377_b200.dist import RankStats, gather_stats, max_over_ranks as _mor
+
     def max_over_ranks(x):
-        if world > 1:
-            t = torch.tensor([x], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            return float(t.item())
-        return x
+        return _mor(x, device=dev)
 
     for _ in range(args.warmup):
         cycle()
@@ -362,6 +360,10 @@ def run_b200(args, cfg, world, rank, local):
                   "attention_us_per_layer_p50": round(statistics.median(at) * 1e3, 2),
                   "attention_gbs": round(k3_bytes / (statistics.median(at) * 1e-3) / 1e9, 1)}
 
+    st = eng.stats()
+    ranks = gather_stats(RankStats(rank=rank, tables=n_tab, tokens_scored=int(st.tokens_scored),
+                                   pages_evicted=int(st.pages_evicted),
+                                   algorithmic_bytes=int(step_bytes * args.steps), kernel_ms=k2_ms))
     cpu = cpu_baseline(cfg, args) if (rank == 0 and world == 1 and not args.no_cpu) else None
     if rank == 0:
         line = {
@@ -386,6 +388,7 @@ def run_b200(args, cfg, world, rank, local):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "ranks": ranks if world > 1 else None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
