@@ -299,26 +299,19 @@ int peo_prefill(peo_engine* e, int32_t layer, const void* k, const void* v,
     return ST_OK;
 }
 
+/* Appends run serially in ascending table id, like the reference's loop of
+ * append_token calls (block_table.cpp:10-19): the first pop that finds the
+ * free list empty fails with PoolExhausted (page_pool.cpp:26-28) and stops
+ * the launch (later tables are not appended). A popping table already at
+ * max_pages is skipped with PE_INVALID_STATE. Errors are sticky in
+ * e->status; the first one is returned. */
 int peo_decode_append(peo_engine* e, int32_t layer_begin, int32_t n_layers, const void* k,
                       const void* v, const int64_t* positions) {
     const int32_t H = e->n_tab_heads, B = e->page_size, w = e->width, S = e->n_seqs;
     const size_t es = esize(e->dtype);
     if (layer_begin < 0 || n_layers <= 0 || layer_begin + n_layers > e->n_layers)
         return ST_INVALID_ARG;
-    /* pre-check: pops and table capacity */
-    int64_t need = 0;
-    for (int32_t s = 0; s < S; ++s)
-        for (int32_t l = layer_begin; l < layer_begin + n_layers; ++l)
-            for (int32_t h = 0; h < H; ++h) {
-                const int32_t t = peo_table_id(e, s, l, h);
-                const int pop = e->num_pages[t] == 0 || e->newest_fill[t] == B;
-                if (pop && e->num_pages[t] >= e->max_pages) return ST_INVALID_STATE;
-                need += pop;
-            }
-    if (need > e->top) {
-        e->status = ST_POOL_EXHAUSTED;
-        return ST_POOL_EXHAUSTED;
-    }
+    int rc = ST_OK;
     /* ascending table id == seq-major, then layer, then head */
     for (int32_t s = 0; s < S; ++s)
         for (int32_t l = layer_begin; l < layer_begin + n_layers; ++l)
@@ -328,6 +321,16 @@ int peo_decode_append(peo_engine* e, int32_t layer_begin, int32_t n_layers, cons
                 const uint8_t* kr = (const uint8_t*)k + off;
                 const uint8_t* vr = (const uint8_t*)v + off;
                 if (e->num_pages[t] == 0 || e->newest_fill[t] == B) {
+                    if (e->num_pages[t] >= e->max_pages) {
+                        if (!e->status) e->status = ST_INVALID_STATE;
+                        if (!rc) rc = ST_INVALID_STATE;
+                        continue;
+                    }
+                    if (e->top == 0) {
+                        if (!e->status) e->status = ST_POOL_EXHAUSTED;
+                        if (!rc) rc = ST_POOL_EXHAUSTED;
+                        return rc;
+                    }
                     const int32_t page = e->stack[--e->top];
                     e->block_table[(size_t)t * e->max_pages + e->num_pages[t]] = page;
                     e->num_pages[t] += 1;
@@ -339,7 +342,7 @@ int peo_decode_append(peo_engine* e, int32_t layer_begin, int32_t n_layers, cons
                 e->newest_fill[t] += 1;
                 e->retained[t] += 1;
             }
-    return ST_OK;
+    return rc;
 }
 
 int peo_decode_evict(peo_engine* e, int32_t layer_begin, int32_t n_layers, int32_t* victims) {

@@ -89,7 +89,8 @@ int peo_prefill(peo_engine* e, int32_t layer, const void* k, const void* v,
 /* Decode append of one token per table for layers [layer_begin,
  * layer_begin+n_layers): rows [n_layers][n_seqs][n_tab_heads][w]; position
  * per sequence. BlockTable::append_token (block_table.cpp:10-19) with the
- * LIFO PagePool::allocate (page_pool.cpp:24-33). */
+ * LIFO PagePool::allocate (page_pool.cpp:24-33), serially in ascending table
+ * id: the first failing pop stops the launch (PoolExhausted). */
 int peo_decode_append(peo_engine* e, int32_t layer_begin, int32_t n_layers, const void* k,
                       const void* v, const int64_t* positions);
 

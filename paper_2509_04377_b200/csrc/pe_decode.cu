@@ -1,5 +1,4 @@
 // Decode-time kernels of the B200 PagedEviction engine:
-//   plan_kernel          canonical-order free-list planning for one launch
 //   append_kernel        K0: BlockTable::append_token for every table of the launch
 //   evict_score_kernel   K2: recompute page scores from resident K/V bytes, last CTA per
 //                        table takes the argmin and evicts (PagedEvictionPolicy::evict)
@@ -10,77 +9,35 @@
 namespace pe {
 
 // ---------------------------------------------------------------------------
-// plan_kernel: one CTA. Flags every table of the launch, ranks the flags in
-// ascending table id (exclusive scan) and reserves the free-stack range.
-//   APPEND: flag = the append opens a page (no page, or newest write-full:
-//           block_table.cpp:12) -> pops, LIFO from the top (page_pool.cpp:29-31)
-//   EVICT:  flag = PagedEviction trigger (newest write-full && retained > C:
-//           policy.cpp:147-150) -> pushes (page_pool.cpp:37)
-// Pops of one launch precede its pushes.
-__global__ void __launch_bounds__(1024) plan_kernel(DevState s, TableSet ts, int mode,
-                                                     int32_t* rank, int32_t* work,
-                                                     int32_t* victims, LaunchCtl* ctl) {
-    __shared__ int sm[33];
-    __shared__ int bad;
-    const int n = ts.size(s);
-    const int per = (n + blockDim.x - 1) / blockDim.x;
-    const int lo = min(n, (int)threadIdx.x * per);
-    const int hi = min(n, lo + per);
-    if (threadIdx.x == 0) bad = 0;
-    __syncthreads();
-    int cnt = 0;
-    for (int i = lo; i < hi; ++i) {
-        const int t = ts.table(s, i);
-        const int np = s.num_pages[t];
-        int f;
-        if (mode == kPlanAppend) {
-            f = (np == 0 || s.newest_fill[t] == s.B) ? 1 : 0;
-            if (f && np >= s.max_pages) atomicOr(&bad, 1);
-        } else {
-            f = (s.policy == PE_POLICY_PAGED_EVICTION && np > 0 && s.newest_fill[t] == s.B &&
-                 s.retained[t] > s.C) ? 1 : 0;
-        }
-        cnt += f;
-    }
-    int total;
-    int base = block_excl_scan(cnt, sm, &total);
-    for (int i = lo; i < hi; ++i) {
-        const int t = ts.table(s, i);
-        const int np = s.num_pages[t];
-        int f;
-        if (mode == kPlanAppend) {
-            f = (np == 0 || s.newest_fill[t] == s.B) ? 1 : 0;
-        } else {
-            f = (s.policy == PE_POLICY_PAGED_EVICTION && np > 0 && s.newest_fill[t] == s.B &&
-                 s.retained[t] > s.C) ? 1 : 0;
-            if (victims) victims[i] = -1;
-        }
-        rank[i] = f ? base : -1;
-        if (f && work) work[base] = i;
-        base += f;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int top = *s.top;
-        if (mode == kPlanAppend) {
-            if (bad) {
-                set_status(s.status, PE_INVALID_STATE);
-                ctl->abort = 1;
-            } else if (total > top) {
-                set_status(s.status, PE_POOL_EXHAUSTED);  // PoolExhausted, page_pool.cpp:26-28
-                ctl->abort = 1;
-            } else {
-                ctl->abort = 0;
-                ctl->pop_base = top;
-                *s.top = top - total;
-            }
-        } else {
-            ctl->abort = 0;
-            ctl->push_base = top;
-            ctl->count = total;
-            *s.top = top + total;
-        }
-    }
+// Single-pass canonical pop ranks for an append launch (decoupled look-back):
+// CTAs take logical ids from a ticket counter (so a CTA only ever waits on
+// CTAs that already started); logical CTA 0 publishes the stack top, every
+// CTA publishes its pop count and looks back over its predecessors for its
+// exclusive prefix, and the last CTA moves the stack top. Status words:
+// epoch << 32 | flag << 30 | value.
+//
+// Pool exhaustion follows the reference's serial semantics: appends run in
+// ascending table id; the first table whose pop finds the stack empty fails
+// (PoolExhausted, page_pool.cpp:26-28) and no later table of the launch is
+// appended (the exception would have stopped the loop).
+constexpr unsigned long long kLbAgg = 1ull << 30;
+constexpr unsigned long long kLbInc = 2ull << 30;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_i32(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -96,44 +53,101 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
                                                                  const uint8_t* __restrict__ k_rows,
                                                                  const uint8_t* __restrict__ v_rows,
                                                                  const int64_t* __restrict__ positions,
-                                                                 const int32_t* __restrict__ rank,
-                                                                 const LaunchCtl* __restrict__ ctl) {
-    if (ctl->abort) return;
+                                                                 unsigned long long* lb_status, LaunchCtl* ctl,
+                                                                 unsigned long long ticket_base, int epoch) {
+    __shared__ int sh_lid, sh_warp_cnt[kAppendThreads / 32], sh_prefix, sh_pop_base;
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
+    const int nw = kAppendThreads / 32;
     const int n = ts.size(s);
-    const int i0 = (blockIdx.x * (kAppendThreads / 32) + wid) * 16;
-    if (i0 >= n) return;
+    const int n_ctas = (n + 16 * nw - 1) / (16 * nw);
+    if (threadIdx.x == 0) sh_lid = static_cast<int>(atomicAdd(s.grid_ctr, 1ull) - ticket_base);
+    __syncthreads();
+    const int lid = sh_lid;
+    const int i0 = (lid * nw + wid) * 16;
     const int my_i = i0 + (lane >> 1);
     const bool has = my_i < n;
     const int q = lane & 1;
 
-    int t = 0, page = 0, slot = 0, np = 0, rk = -1;
+    int t = 0, np = 0, slot = 0;
+    bool pop = false;
+    bool live = has;
     if (has) {
         t = ts.table(s, my_i);
         np = s.num_pages[t];
-        rk = rank[my_i];
-        if (rk >= 0) {
-            page = s.stack[ctl->pop_base - 1 - rk];
+        slot = s.newest_fill[t];
+        pop = (np == 0 || slot == s.B);
+        if (pop && np >= s.max_pages) {  // table full (max_pages_per_table): skipped
+            if (q == 0) set_status(s.status, PE_INVALID_STATE);
+            pop = false;
+            live = false;
+        }
+    }
+    const unsigned pop_mask = __ballot_sync(0xFFFFFFFFu, pop && q == 0);
+    if (lane == 0) sh_warp_cnt[wid] = __popc(pop_mask);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int local = 0;
+        for (int w = 0; w < nw; ++w) local += sh_warp_cnt[w];
+        const unsigned long long ep = static_cast<unsigned long long>(static_cast<unsigned>(epoch)) << 32;
+        int prefix = 0;
+        if (lid == 0) {
+            const int top = *s.top;
+            ctl->pop_base = top;
+            st_release_u64(lb_status, ep | kLbInc | static_cast<unsigned long long>(local));
+            st_release_i32(&ctl->ready, epoch);
+            sh_pop_base = top;
+        } else {
+            st_release_u64(lb_status + lid, ep | kLbAgg | static_cast<unsigned long long>(local));
+            for (int j = lid - 1; j >= 0;) {
+                const unsigned long long w = ld_acquire_u64(lb_status + j);
+                if ((w >> 32) != static_cast<unsigned>(epoch)) continue;  // predecessor not yet published
+                prefix += static_cast<int>(w & ((1ull << 30) - 1));
+                if (w & kLbInc) break;
+                --j;
+            }
+            st_release_u64(lb_status + lid, ep | kLbInc | static_cast<unsigned long long>(prefix + local));
+            while (ld_acquire_i32(&ctl->ready) != epoch) __nanosleep(32);
+            sh_pop_base = ctl->pop_base;
+        }
+        if (lid == n_ctas - 1) {
+            const int total = prefix + local;
+            *s.top = sh_pop_base - min(total, sh_pop_base);
+        }
+        sh_prefix = prefix;
+    }
+    __syncthreads();
+    // rank of this table's pop among the launch's pops (ascending table id);
+    // for a non-popping table: the number of pops before it
+    int rank = sh_prefix;
+    for (int w = 0; w < wid; ++w) rank += sh_warp_cnt[w];
+    rank += __popc(pop_mask & ((1u << (lane & ~1)) - 1u));
+    const int top = sh_pop_base;
+    if (pop && rank == top && q == 0) set_status(s.status, PE_POOL_EXHAUSTED);  // first failing pop
+    const bool served = live && (pop ? rank < top : rank <= top);
+
+    int page = 0;
+    if (served) {
+        if (pop) {
+            page = s.stack[top - 1 - rank];
             slot = 0;
         } else {
             page = s.block_table[(int64_t)t * s.max_pages + np - 1];
-            slot = s.newest_fill[t];
         }
     }
-    __syncwarp();  // both lanes of a pair read the table state before lane 0 updates it
-    if (has && q == 0 && rk >= 0) {
+    __syncwarp();
+    if (served && q == 0 && pop) {
         s.block_table[(int64_t)t * s.max_pages + np] = page;
         s.num_pages[t] = np + 1;
     }
-    const int64_t in_row = has ? ts.input_row(s, my_i) : 0;
+    const int64_t in_row = served ? ts.input_row(s, my_i) : 0;
     const uint8_t* krow = k_rows + in_row * s.row_bytes;
     const uint8_t* vrow = v_rows + in_row * s.row_bytes;
     uint8_t* kdst = s.pages + (((int64_t)page * 2 + 0) * s.B + slot) * s.pitch;
     uint8_t* vdst = s.pages + (((int64_t)page * 2 + 1) * s.B + slot) * s.pitch;
-    const double S = pair_token_score<SV>(krow, vrow, has, s.w, s.dtype, has ? kdst : nullptr,
-                                          has ? vdst : nullptr);
-    if (has && q == 0) {
+    const double S = pair_token_score<SV>(krow, vrow, served, s.w, s.dtype, served ? kdst : nullptr,
+                                          served ? vdst : nullptr);
+    if (served && q == 0) {
         const int64_t ps = (int64_t)page * s.B + slot;
         s.positions[ps] = static_cast<int32_t>(positions[ts.input_row(s, my_i) / s.tab_heads % s.n_seqs]);
         s.token_scores[ps] = S;
@@ -147,17 +161,17 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
             s.page_scores[page] = sum / static_cast<double>(s.B);
         }
     }
+    (void)nw;
 }
 
 // ---------------------------------------------------------------------------
 // Finalisation of one evicting table (shared by K2 and K2c), executed by one
 // warp: rank_pages argmin (strict <, ties -> smaller index, importance.cpp:62-75),
-// free_page (retained -= fill; erase -> entries shift left, block_table.cpp:21-31),
-// release = push on the free stack at the canonical rank (page_pool.cpp:35-38).
-__device__ __forceinline__ void finalize_evict(const DevState& s, int t, int i, int N,
-                                               const double* scores, const int32_t* rank,
-                                               const LaunchCtl* ctl, int32_t* victims,
-                                               int32_t* /*unused*/) {
+// free_page (retained -= fill; erase -> entries shift left, block_table.cpp:21-31).
+// The released page id is parked in vpage[i]; the grid's last CTA pushes all
+// of them on the free stack in ascending table id (push_victims below).
+__device__ __forceinline__ void finalize_evict(const DevState& s, int t, int i, int N, const double* scores,
+                                               int32_t* vpage, int32_t* victims) {
     const int lane = threadIdx.x & 31;
     double best = 0.0;
     int bj = 0x7FFFFFFF;
@@ -192,138 +206,184 @@ __device__ __forceinline__ void finalize_evict(const DevState& s, int t, int i, 
         s.num_pages[t] = N - 1;
         s.retained[t] -= s.B;  // every page is full when the trigger fires
         s.newest_fill[t] = (N - 1 > 0) ? s.B : 0;
-        s.stack[ctl->push_base + rank[i]] = victim_page;
+        vpage[i] = victim_page;
         if (victims) victims[i] = victim;
         atomicAdd(s.evict_count, 1ull);
     }
     __syncwarp();
 }
 
+// PagedEviction trigger, policy.cpp:147-150: newest page write-full and
+// retained > C (num_pages > 0 implied).
+__device__ __forceinline__ bool evict_triggered(const DevState& s, int t) {
+    return s.policy == PE_POLICY_PAGED_EVICTION && s.num_pages[t] > 0 && s.newest_fill[t] == s.B &&
+           s.retained[t] > s.C;
+}
+
+// Grid-level completion: every CTA takes a ticket when it is done; the last
+// one pushes the launch's released pages on the free stack in ascending
+// table id (release, page_pool.cpp:35-38; canonical order DESIGN.md §1.6).
+__device__ __forceinline__ void push_victims_if_last(const DevState& s, int n, int32_t* vpage,
+                                                     unsigned long long grid_last) {
+    __shared__ int is_last;
+    __shared__ int scan_sm[33];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = (atomicAdd(s.grid_ctr, 1ull) == grid_last);
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int lo = min(n, (int)threadIdx.x * per);
+    const int hi = min(n, lo + per);
+    int cnt = 0;
+    for (int i = lo; i < hi; ++i) cnt += __ldcg(vpage + i) >= 0;
+    int total;
+    int k = block_excl_scan(cnt, scan_sm, &total);
+    const int top = *s.top;
+    for (int i = lo; i < hi; ++i) {
+        const int pg = __ldcg(vpage + i);
+        if (pg >= 0) s.stack[top + k++] = pg;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *s.top = top + total;
+}
+
 // ---------------------------------------------------------------------------
-// evict_score_kernel (K2, recompute): grid (work items, chunks). CTA (y, c)
-// scores pages [c*P, c*P+P) of evicting table work[y]; each warp takes whole
+// evict_score_kernel (K2, recompute): grid (launch tables, chunks). CTA (y, c)
+// scores pages [c*P, c*P+P) of table y if it triggers; each warp takes whole
 // pages: lane pair r scores slot r (K row r, V row r of the page, both
 // 256-byte rows read straight into registers), the page mean is the
 // slot-order sum / fill (score_pages -> page_score, importance.cpp:19-39).
-// The last CTA of the table (atomic ticket) takes the argmin and evicts.
+// The last CTA of the table (atomic ticket) takes the argmin and evicts; the
+// last CTA of the grid pushes the released pages.
 template <int SV>
 __global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
-    DevState s, TableSet ts, int pages_per_cta, const int32_t* __restrict__ work,
-    const int32_t* __restrict__ rank, const LaunchCtl* __restrict__ ctl, double* scratch,
-    int32_t* tickets, int32_t* victims) {
+    DevState s, TableSet ts, int pages_per_cta, double* scratch, int32_t* tickets, int32_t* vpage,
+    int32_t* victims, unsigned long long grid_last) {
     __shared__ double page_mean[kMaxPagesPerCta];
     __shared__ int last;
     const int y = blockIdx.x;
-    if (y >= ctl->count) return;
-    const int i = work[y];
-    const int t = ts.table(s, i);
+    const int c = blockIdx.y;
+    const int t = ts.table(s, y);
+    const bool trig = evict_triggered(s, t);
     const int N = s.num_pages[t];
     const int n_cta = (N + pages_per_cta - 1) / pages_per_cta;
-    const int c = blockIdx.y;
-    if (c >= n_cta) return;
-    const int p0 = c * pages_per_cta;
-    const int np = min(pages_per_cta, N - p0);
-    const int lane = threadIdx.x & 31;
-    const int wid = threadIdx.x >> 5;
-    const int nw = blockDim.x >> 5;
-    const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
-    const int64_t page_bytes = (int64_t)2 * s.B * s.pitch;
-
-    if (s.B == 16) {
-        // one 16-slot group per page, read straight into registers (no
-        // prefetch buffer: occupancy, i.e. warps in flight, hides HBM latency)
-        const int slot = lane >> 1;
-        const int64_t ko = (int64_t)slot * s.pitch, vo = (int64_t)(16 + slot) * s.pitch;
-        for (int lp = wid; lp < np; lp += nw) {
-            const uint8_t* base = s.pages + (int64_t)__ldg(row + p0 + lp) * page_bytes;
-            const double S = pair_token_score<SV>(base + ko, base + vo, true, s.w, s.dtype);
-            double sum = 0.0;
+    if (!trig) {
+        if (c == 0 && threadIdx.x == 0) {
+            vpage[y] = -1;
+            if (victims) victims[y] = -1;
+        }
+    } else if (c < n_cta) {
+        const int p0 = c * pages_per_cta;
+        const int np = min(pages_per_cta, N - p0);
+        const int lane = threadIdx.x & 31;
+        const int wid = threadIdx.x >> 5;
+        const int nw = blockDim.x >> 5;
+        const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
+        const int64_t page_bytes = (int64_t)2 * s.B * s.pitch;
+        if (s.B == 16) {
+            // one 16-slot group per page, read straight into registers (no
+            // prefetch buffer: occupancy, i.e. warps in flight, hides HBM latency)
+            const int slot = lane >> 1;
+            const int64_t ko = (int64_t)slot * s.pitch, vo = (int64_t)(16 + slot) * s.pitch;
+            for (int lp = wid; lp < np; lp += nw) {
+                const uint8_t* base = s.pages + (int64_t)__ldg(row + p0 + lp) * page_bytes;
+                const double S = pair_token_score<SV>(base + ko, base + vo, true, s.w, s.dtype);
+                double sum = 0.0;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
-            if (lane == 0) page_mean[lp] = sum / 16.0;
-        }
-    } else {
-        for (int lp = wid; lp < np; lp += nw) {
-            const int id = __ldg(row + p0 + lp);
-            const uint8_t* base = s.pages + (int64_t)id * page_bytes;
-            double sum = 0.0;
-            for (int s0 = 0; s0 < s.B; s0 += 16) {
-                const int slot = s0 + (lane >> 1);
-                const bool valid = slot < s.B;
-                const double S = pair_token_score<SV>(base + (int64_t)slot * s.pitch,
-                                                      base + (int64_t)(s.B + slot) * s.pitch, valid, s.w, s.dtype);
-                const int ns = min(16, s.B - s0);
-                for (int j = 0; j < ns; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+                for (int j = 0; j < 16; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+                if (lane == 0) page_mean[lp] = sum / 16.0;
             }
-            if (lane == 0) page_mean[lp] = sum / static_cast<double>(s.B);
+        } else {
+            for (int lp = wid; lp < np; lp += nw) {
+                const int id = __ldg(row + p0 + lp);
+                const uint8_t* base = s.pages + (int64_t)id * page_bytes;
+                double sum = 0.0;
+                for (int s0 = 0; s0 < s.B; s0 += 16) {
+                    const int slot = s0 + (lane >> 1);
+                    const bool valid = slot < s.B;
+                    const double S = pair_token_score<SV>(base + (int64_t)slot * s.pitch,
+                                                          base + (int64_t)(s.B + slot) * s.pitch, valid, s.w,
+                                                          s.dtype);
+                    const int ns = min(16, s.B - s0);
+                    for (int j = 0; j < ns; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+                }
+                if (lane == 0) page_mean[lp] = sum / static_cast<double>(s.B);
+            }
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < np; j += blockDim.x) scratch[(int64_t)y * s.max_pages + p0 + j] = page_mean[j];
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) last = (atomicAdd(&tickets[y], 1) == n_cta - 1);
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            if (wid == 0) {
+                finalize_evict(s, t, y, N, scratch + (int64_t)y * s.max_pages, vpage, victims);
+                if (lane == 0) tickets[y] = 0;
+            }
         }
     }
-    __syncthreads();
-    for (int j = threadIdx.x; j < np; j += blockDim.x) {
-        scratch[(int64_t)y * s.max_pages + p0 + j] = page_mean[j];
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int tk = atomicAdd(&tickets[y], 1);
-        last = (tk == n_cta - 1);
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    if (wid == 0) {
-        finalize_evict(s, t, i, N, scratch + (int64_t)y * s.max_pages, rank, ctl, victims, nullptr);
-        if (lane == 0) tickets[y] = 0;
-    }
+    push_victims_if_last(s, ts.size(s), vpage, grid_last);
 }
 
 template <int SV>
 void launch_evict_score(dim3 grid, int threads, cudaStream_t st, const DevState& s, const TableSet& ts, int ppc,
-                        const int32_t* work, const int32_t* rank, const LaunchCtl* ctl, double* scratch,
-                        int32_t* tickets, int32_t* victims) {
-    evict_score_kernel<SV><<<grid, threads, 0, st>>>(s, ts, ppc, work, rank, ctl, scratch, tickets, victims);
+                        double* scratch, int32_t* tickets, int32_t* vpage, int32_t* victims,
+                        unsigned long long grid_last) {
+    evict_score_kernel<SV><<<grid, threads, 0, st>>>(s, ts, ppc, scratch, tickets, vpage, victims, grid_last);
 }
 
 template <int SV>
 void launch_append(int blocks, cudaStream_t st, const DevState& s, const TableSet& ts, const uint8_t* k,
-                   const uint8_t* v, const int64_t* pos, const int32_t* rank, const LaunchCtl* ctl) {
-    append_kernel<SV><<<blocks, kAppendThreads, 0, st>>>(s, ts, k, v, pos, rank, ctl);
+                   const uint8_t* v, const int64_t* pos, unsigned long long* lb, LaunchCtl* ctl,
+                   unsigned long long ticket_base, int epoch) {
+    append_kernel<SV><<<blocks, kAppendThreads, 0, st>>>(s, ts, k, v, pos, lb, ctl, ticket_base, epoch);
 }
 
 void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st, const DevState& s,
-                            const TableSet& ts, int ppc, const int32_t* work, const int32_t* rank,
-                            const LaunchCtl* ctl, double* scratch, int32_t* tickets, int32_t* victims) {
-    PE_SCORE_DISPATCH(variant, (launch_evict_score<SV>(grid, threads, st, s, ts, ppc, work, rank, ctl, scratch,
-                                                        tickets, victims)));
+                            const TableSet& ts, int ppc, double* scratch, int32_t* tickets, int32_t* vpage,
+                            int32_t* victims, unsigned long long grid_last) {
+    PE_SCORE_DISPATCH(variant, (launch_evict_score<SV>(grid, threads, st, s, ts, ppc, scratch, tickets, vpage,
+                                                        victims, grid_last)));
 }
 
 void launch_append_any(int variant, int blocks, cudaStream_t st, const DevState& s, const TableSet& ts,
-                       const uint8_t* k, const uint8_t* v, const int64_t* pos, const int32_t* rank,
-                       const LaunchCtl* ctl) {
-    PE_SCORE_DISPATCH(variant, (launch_append<SV>(blocks, st, s, ts, k, v, pos, rank, ctl)));
+                       const uint8_t* k, const uint8_t* v, const int64_t* pos, unsigned long long* lb,
+                       LaunchCtl* ctl, unsigned long long ticket_base, int epoch) {
+    PE_SCORE_DISPATCH(variant, (launch_append<SV>(blocks, st, s, ts, k, v, pos, lb, ctl, ticket_base, epoch)));
 }
 
 // ---------------------------------------------------------------------------
-// evict_cached_kernel (K2c): one warp per work item; page means were cached
-// when each page filled, so the decision reads N doubles (gathered through
-// the block table) instead of N pages. Bit-identical to K2.
-__global__ void __launch_bounds__(256) evict_cached_kernel(DevState s, TableSet ts,
-                                                           const int32_t* __restrict__ work,
-                                                           const int32_t* __restrict__ rank,
-                                                           const LaunchCtl* __restrict__ ctl,
-                                                           double* scratch, int32_t* victims) {
+// evict_cached_kernel (K2c): one warp per launch table; page means were
+// cached when each page filled, so the decision reads N doubles (gathered
+// through the block table) instead of N pages. Bit-identical to K2.
+__global__ void __launch_bounds__(256) evict_cached_kernel(DevState s, TableSet ts, double* scratch,
+                                                           int32_t* vpage, int32_t* victims,
+                                                           unsigned long long grid_last) {
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int y = blockIdx.x * 8 + wid;
-    if (y >= ctl->count) return;
-    const int i = work[y];
-    const int t = ts.table(s, i);
-    const int N = s.num_pages[t];
-    const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
-    double* sc = scratch + (int64_t)y * s.max_pages;
-    for (int j = lane; j < N; j += 32) sc[j] = s.page_scores[row[j]];
-    __syncwarp();
-    finalize_evict(s, t, i, N, sc, rank, ctl, victims, nullptr);
+    const int n = ts.size(s);
+    if (y < n) {
+        const int t = ts.table(s, y);
+        if (!evict_triggered(s, t)) {
+            if (lane == 0) {
+                vpage[y] = -1;
+                if (victims) victims[y] = -1;
+            }
+        } else {
+            const int N = s.num_pages[t];
+            const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
+            double* sc = scratch + (int64_t)y * s.max_pages;
+            for (int j = lane; j < N; j += 32) sc[j] = s.page_scores[row[j]];
+            __syncwarp();
+            finalize_evict(s, t, y, N, sc, vpage, victims);
+        }
+    }
+    push_victims_if_last(s, n, vpage, grid_last);
 }
 
 }  // namespace pe

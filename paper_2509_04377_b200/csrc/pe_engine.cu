@@ -60,6 +60,10 @@ struct pe_engine {
     int32_t* work = nullptr;
     int32_t* victims = nullptr;
     int32_t* tickets = nullptr;
+    int32_t* vpage = nullptr;           // per launch table released page id (or -1)
+    unsigned long long* lb_status = nullptr;  // append look-back status words (one per CTA)
+    int append_epoch = 0;
+    unsigned long long grid_tickets = 0;  // host mirror of DevState::grid_ctr
     double* evict_scratch = nullptr;
     int32_t* tab_len = nullptr;
     int64_t* tab_tok0 = nullptr;
@@ -69,6 +73,8 @@ struct pe_engine {
     int64_t* h_tab_keybase = nullptr;   // pinned
     unsigned long long* keys = nullptr;
     size_t keys_elems = 0;
+    int32_t* surv = nullptr;
+    size_t surv_elems = 0;
     int variant = 0;
     int32_t* h_tab_len = nullptr;       // pinned
     int64_t* h_tab_tok0 = nullptr;      // pinned
@@ -253,7 +259,9 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         dalloc(&s.num_pages, n_tables) != cudaSuccess || dalloc(&s.newest_fill, n_tables) != cudaSuccess ||
         dalloc(&s.retained, n_tables) != cudaSuccess || dalloc(&s.stack, (size_t)cap) != cudaSuccess ||
         dalloc(&s.top, 1) != cudaSuccess || dalloc(&s.status, 1) != cudaSuccess ||
-        dalloc(&s.evict_count, 1) != cudaSuccess || dalloc(&e->ctl, 1) != cudaSuccess ||
+        dalloc(&s.evict_count, 1) != cudaSuccess || dalloc(&s.grid_ctr, 1) != cudaSuccess ||
+        dalloc(&e->vpage, n_tables) != cudaSuccess || dalloc(&e->ctl, 1) != cudaSuccess ||
+        dalloc(&e->lb_status, (size_t)n_tables / 64 + 2) != cudaSuccess ||
         dalloc(&e->rank, n_tables) != cudaSuccess || dalloc(&e->work, n_tables) != cudaSuccess ||
         dalloc(&e->victims, n_tables) != cudaSuccess || dalloc(&e->tickets, n_tables) != cudaSuccess ||
         dalloc(&e->evict_scratch, (size_t)n_tables * max_pages) != cudaSuccess ||
@@ -286,7 +294,10 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             cudaMemset(s.retained, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
             cudaMemset(s.status, 0, sizeof(int32_t)) != cudaSuccess ||
             cudaMemset(s.evict_count, 0, sizeof(unsigned long long)) != cudaSuccess ||
+            cudaMemset(s.grid_ctr, 0, sizeof(unsigned long long)) != cudaSuccess ||
             cudaMemset(e->tickets, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
+            cudaMemset(e->lb_status, 0, sizeof(unsigned long long) * ((size_t)n_tables / 64 + 2)) != cudaSuccess ||
+            cudaMemset(e->ctl, 0, sizeof(LaunchCtl)) != cudaSuccess ||
             cudaMemset(s.positions, 0xFF, sizeof(int32_t) * (size_t)cap * s.B) != cudaSuccess ||
             cudaMemset(s.pages, 0, (size_t)cap * page_bytes) != cudaSuccess ||
             cudaDeviceSynchronize() != cudaSuccess) {
@@ -305,7 +316,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, *out) == cudaSuccess;
         };
         int mma64 = 0, mma128 = 0;
-        if (!allow(reinterpret_cast<const void*>(prefill_pack_kernel), &e->max_dyn_prefill) ||
+        if (!allow(reinterpret_cast<const void*>(prefill_select_kernel), &e->max_dyn_prefill) ||
             !allow(reinterpret_cast<const void*>(attention_split_kernel), &e->max_dyn_attn) ||
             !allow(attention_mma_fn(64), &mma64) || !allow(attention_mma_fn(128), &mma128)) {
             cudaGetLastError();
@@ -322,10 +333,11 @@ pe_status pe_engine_destroy(pe_engine* e) {
     cudaDeviceSynchronize();
     DevState& s = e->s;
     void* dev[] = {s.pages, s.positions, s.token_scores, s.page_scores, s.block_table, s.num_pages,
-                   s.newest_fill, s.retained, s.stack, s.top, s.status, s.evict_count, e->ctl, e->rank,
+                   s.newest_fill, s.retained, s.stack, s.top, s.status, s.evict_count, s.grid_ctr, e->vpage,
+                   e->ctl, e->rank,
                    e->work, e->victims, e->tickets, e->evict_scratch, e->tab_len, e->tab_tok0,
                    e->tab_pagebase, e->evicted_dev, e->stage_a, e->stage_b, e->stage_c, e->part_o,
-                   e->part_ml, e->out_stage, e->tab_keybase, e->keys};
+                   e->part_ml, e->out_stage, e->tab_keybase, e->keys, e->surv, e->lb_status};
     for (void* p : dev) {
         if (p) cudaFree(p);
     }
@@ -375,7 +387,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
         }
     }
     const int chunk_cap = (max_len + kPrefillCluster - 1) / kPrefillCluster;
-    const size_t pack_smem = (size_t)chunk_cap * 12;
+    const size_t pack_smem = (size_t)chunk_cap * 8;
     if (pack_smem > (size_t)e->max_dyn_prefill)
         return fail(PE_INVALID_ARG, "prefill length " + std::to_string(max_len) +
                                         " exceeds the per-cluster shared-memory capacity");
@@ -387,6 +399,8 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     r = as_device(e, v, in_bytes, &e->stage_b, &e->stage_b_bytes, st, &dv);
     if (r != PE_OK) return r;
     r = ensure_t(&e->keys, &e->keys_elems, (size_t)total_keys);
+    if (r != PE_OK) return r;
+    r = ensure_t(&e->surv, &e->surv_elems, (size_t)total_pages * s.B);
     if (r != PE_OK) return r;
     PE_CUDA(cudaMemcpyAsync(e->tab_len, e->h_tab_len, sizeof(int32_t) * n_tab, cudaMemcpyHostToDevice, st));
     PE_CUDA(cudaMemcpyAsync(e->tab_tok0, e->h_tab_tok0, sizeof(int64_t) * n_tab, cudaMemcpyHostToDevice, st));
@@ -403,6 +417,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     a.evicted_counts = evicted_counts ? (ev_dev ? evicted_counts : e->evicted_dev) : nullptr;
     a.keys = e->keys;
     a.tab_keybase = e->tab_keybase;
+    a.surv = e->surv;
     a.n_tab = n_tab;
     a.seq_begin = seq_begin;
     a.layer = layer;
@@ -411,10 +426,12 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     plan_prefill_kernel<<<1, 1024, 0, st>>>(s, a, static_cast<int32_t>(total_pages), e->ctl);
     launch_prefill_score_any(e->variant, dim3((max_len + kScoreTokensPerCta - 1) / kScoreTokensPerCta, n_seqs), st, s,
                              a, e->ctl);
-    prefill_pack_kernel<<<dim3(kPrefillCluster, n_tab), kPackThreads, pack_smem, st>>>(s, a, e->ctl);
+    prefill_select_kernel<<<dim3(kPrefillCluster, n_tab), kPackThreads, pack_smem, st>>>(s, a, e->ctl);
+    const int max_keep_pages = (std::min(max_len, s.policy == PE_POLICY_PAGED_EVICTION ? s.C : max_len) + s.B - 1) / s.B;
+    prefill_copy_kernel<<<dim3((max_keep_pages + 3) / 4, n_tab), 128, 0, st>>>(s, a, e->ctl);
     r = check_launch(e, "prefill_kernel");
     if (r != PE_OK) return r;
-    e->stats.kernel_launches += 3;
+    e->stats.kernel_launches += 4;
     e->stats.prefill_calls += 1;
     e->stats.tokens_scored += (int64_t)tokens * H;
     if (evicted_counts && !ev_dev) {
@@ -442,13 +459,17 @@ pe_status pe_decode_append(pe_engine* e, int32_t layer_begin, int32_t n_layers, 
     if (r != PE_OK) return r;
     r = as_device(e, positions, sizeof(int64_t) * s.n_seqs, &e->stage_c, &e->stage_c_bytes, st, &dp);
     if (r != PE_OK) return r;
-    plan_kernel<<<1, 1024, 0, st>>>(s, ts, kPlanAppend, e->rank, nullptr, nullptr, e->ctl);
+    // one launch: canonical pop ranks by a single-pass decoupled look-back
     const int warps = kAppendThreads / 32;
     const int blocks = (n + 16 * warps - 1) / (16 * warps);
-    launch_append_any(e->variant, blocks, st, s, ts, dk, dv, reinterpret_cast<const int64_t*>(dp), e->rank, e->ctl);
+    const unsigned long long ticket_base = e->grid_tickets;
+    e->grid_tickets += blocks;
+    e->append_epoch = (e->append_epoch % 0x3FFFFFFF) + 1;
+    launch_append_any(e->variant, blocks, st, s, ts, dk, dv, reinterpret_cast<const int64_t*>(dp), e->lb_status,
+                      e->ctl, ticket_base, e->append_epoch);
     r = check_launch(e, "append_kernel");
     if (r != PE_OK) return r;
-    e->stats.kernel_launches += 2;
+    e->stats.kernel_launches += 1;
     e->stats.append_calls += 1;
     return PE_OK;
 }
@@ -468,19 +489,23 @@ pe_status pe_decode_evict(pe_engine* e, int32_t layer_begin, int32_t n_layers, i
     const int n = ts.size(s);
     const bool vic_dev = victims && is_device_ptr(victims);
     int32_t* vdst = vic_dev ? victims : e->victims;
-    plan_kernel<<<1, 1024, 0, st>>>(s, ts, kPlanEvict, e->rank, e->work, vdst, e->ctl);
-    const int ymax = n;
+    // one launch: the grid's last CTA pushes the released pages in ascending
+    // table id (no separate planner)
     if (mode == PE_SCORE_RECOMPUTE) {
         const int chunks = (s.max_pages + kEvictPagesPerCta - 1) / kEvictPagesPerCta;
-        launch_evict_score_any(e->variant, dim3(ymax, chunks), kEvictThreads, st, s, ts, kEvictPagesPerCta, e->work,
-                               e->rank, e->ctl, e->evict_scratch, e->tickets, vdst);
+        const unsigned long long grid = (unsigned long long)n * chunks;
+        e->grid_tickets += grid;
+        launch_evict_score_any(e->variant, dim3(n, chunks), kEvictThreads, st, s, ts, kEvictPagesPerCta,
+                               e->evict_scratch, e->tickets, e->vpage, vdst, e->grid_tickets - 1);
     } else {
-        evict_cached_kernel<<<(ymax + 7) / 8, 256, 0, st>>>(s, ts, e->work, e->rank, e->ctl,
-                                                           e->evict_scratch, vdst);
+        const unsigned long long grid = (unsigned long long)(n + 7) / 8;
+        e->grid_tickets += grid;
+        evict_cached_kernel<<<(n + 7) / 8, 256, 0, st>>>(s, ts, e->evict_scratch, e->vpage, vdst,
+                                                          e->grid_tickets - 1);
     }
     pe_status r = check_launch(e, "evict kernel");
     if (r != PE_OK) return r;
-    e->stats.kernel_launches += 2;
+    e->stats.kernel_launches += 1;
     e->stats.evict_calls += 1;
     if (victims && !vic_dev) {
         PE_CUDA(cudaMemcpyAsync(victims, e->victims, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));

@@ -32,6 +32,7 @@ struct DevState {
     int32_t* top;
     int32_t* status;
     unsigned long long* evict_count;
+    unsigned long long* grid_ctr;   // monotonically increasing CTA completion tickets
     int32_t capacity, B, C, w, pitch, row_bytes, max_pages, n_tables;
     int32_t n_seqs, n_layers, tab_heads, dtype, policy;
 };
@@ -42,6 +43,8 @@ struct LaunchCtl {
     int32_t pop_base;   // stack top before this launch's pops
     int32_t push_base;  // stack top before this launch's pushes
     int32_t count;      // number of flagged tables (evict work items)
+    int32_t ready;      // epoch of the launch whose fields are valid (append look-back)
+    int32_t pad_;
 };
 
 // Launch table set: decode launches cover every sequence for layers

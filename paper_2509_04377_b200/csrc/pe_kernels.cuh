@@ -6,15 +6,12 @@
 
 namespace pe {
 
-constexpr int kPlanAppend = 0;
-constexpr int kPlanEvict = 1;
-
 constexpr int kAppendThreads = 128;      // 4 warps x 16 tables
 constexpr int kEvictThreads = 128;       // 4 warps per CTA
 constexpr int kMaxPagesPerCta = 64;
 constexpr int kPrefillThreads = 128;     // score kernel: 4 warps per CTA
 constexpr int kScoreTokensPerCta = 256;  // tokens (x all heads) per score CTA
-constexpr int kPackThreads = 256;        // select/pack kernel: 8 warps per CTA
+constexpr int kPackThreads = 256;        // select kernel: 8 warps per CTA
 constexpr int kPrefillCluster = 8;       // CTAs per table (portable cluster size)
 
 struct PrefillArgs {
@@ -27,26 +24,25 @@ struct PrefillArgs {
     int32_t* evicted_counts;             // [n_tab] or nullptr
     unsigned long long* keys;            // score keys, table i at tab_keybase[i]
     const int64_t* tab_keybase;          // [n_tab] exclusive prefix of L
+    int32_t* surv;                       // survivor token indices, table i at tab_pagebase[i]*B
     int32_t n_tab;
     int32_t seq_begin, layer;
     int32_t chunk_cap;                   // max tokens per CTA (keys smem capacity)
 };
 
-__global__ void plan_kernel(DevState s, TableSet ts, int mode, int32_t* rank, int32_t* work,
-                            int32_t* victims, LaunchCtl* ctl);
-__global__ void evict_cached_kernel(DevState s, TableSet ts, const int32_t* work,
-                                    const int32_t* rank, const LaunchCtl* ctl, double* scratch,
-                                    int32_t* victims);
+__global__ void evict_cached_kernel(DevState s, TableSet ts, double* scratch, int32_t* vpage, int32_t* victims,
+                                    unsigned long long grid_last);
 __global__ void plan_prefill_kernel(DevState s, PrefillArgs a, int32_t total_pages, LaunchCtl* ctl);
-__global__ void prefill_pack_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
+__global__ void prefill_select_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
+__global__ void prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 
 // host-side launchers of the row-geometry-specialised kernels (pe_score.cuh variants)
 void launch_append_any(int variant, int blocks, cudaStream_t st, const DevState& s, const TableSet& ts,
-                       const uint8_t* k, const uint8_t* v, const int64_t* pos, const int32_t* rank,
-                       const LaunchCtl* ctl);
+                       const uint8_t* k, const uint8_t* v, const int64_t* pos, unsigned long long* lb,
+                       LaunchCtl* ctl, unsigned long long ticket_base, int epoch);
 void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st, const DevState& s,
-                            const TableSet& ts, int ppc, const int32_t* work, const int32_t* rank,
-                            const LaunchCtl* ctl, double* scratch, int32_t* tickets, int32_t* victims);
+                            const TableSet& ts, int ppc, double* scratch, int32_t* tickets, int32_t* vpage,
+                            int32_t* victims, unsigned long long grid_last);
 void launch_prefill_score_any(int variant, dim3 grid, cudaStream_t st, const DevState& s, const PrefillArgs& a,
                               const LaunchCtl* ctl);
 

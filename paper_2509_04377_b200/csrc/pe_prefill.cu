@@ -13,7 +13,7 @@
 //               launch (lane pair per token, exact fp64 certificate scoring,
 //               pe_score.cuh); key = IEEE bits of S (S >= +0 so the u64 order
 //               is the double order), 8 B per token to a key buffer.
-//  select/compact/pack run in prefill_pack_kernel, one cluster of 8 CTAs per
+//  select/compact run in prefill_select_kernel, one cluster of 8 CTAs per
 //  table, CTA r owning tokens [L*r/8, L*(r+1)/8) whose keys it loads to smem:
 //  2. select  — cluster-wide MSB radix select (8-bit digits, histograms merged
 //               through DSMEM) of the E-th smallest key: every key with a
@@ -21,8 +21,9 @@
 //               prefix, the first k_rem in position order (the reference's
 //               position tie rule).
 //  3. compact — block scans + a DSMEM exchange of per-CTA counts give each
-//               survivor its global rank q (position order).
-//  4. pack    — survivor q goes to slot q%B of the table's (q/B)-th page; the
+//               survivor its global rank q (position order) -> survivor list.
+//  4. pack    — prefill_copy_kernel (warp per destination page): survivor q
+//               goes to slot q%B of the table's (q/B)-th page; the
 //               pages are the free-stack entries reserved in canonical order
 //               by plan_prefill_kernel. Token scores and positions are stored
 //               beside the page; full pages get their mean score cached.
@@ -120,7 +121,7 @@ __device__ __forceinline__ void hist_add(uint32_t* hb, uint32_t bin, bool active
 }
 
 __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackThreads)
-    prefill_pack_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
+    prefill_select_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t hist[2][256];
@@ -148,12 +149,10 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackT
     const int h = i % s.tab_heads;
     const int seq = a.seq_begin + i / s.tab_heads;
     const int t = (seq * s.n_layers + a.layer) * s.tab_heads + h;
-    const int64_t row0 = (a.tab_tok0[i] * s.tab_heads + h) * (int64_t)s.row_bytes;
-    const uint8_t* kbase = a.k + row0;
-    const uint8_t* vbase = a.v + row0;
 
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
-    int32_t* list = reinterpret_cast<int32_t*>(smem + (size_t)a.chunk_cap * 8);
+    // survivor q of table i (position order) -> its token index
+    int32_t* surv = a.surv + (int64_t)a.tab_pagebase[i] * s.B;
 
     // ---------------------------------------------------------------- 1. keys -> smem
     {
@@ -282,57 +281,17 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackT
             classify(keys[j], l, tt);
             const bool evict = l || (tt && tr < k_rem);
             tr += tt;
-            if (!evict) list[q_local++] = j;
+            if (!evict) surv[surv_base + q_local++] = lo + j;
         }
     }
     __syncthreads();
 
-    // ---------------------------------------------------------------- 4. pack
-    // The page ids this CTA writes (a contiguous run of the table's pages)
-    // are read once into shared memory; then lane pair r copies survivor
-    // m0 + r: K row and V row with 256-bit loads / stores (a warp moves 16
-    // survivors = 8 KB per step with 8 x 32 B requests in flight per lane).
-    const int pop_base = ctl->pop_base;
-    const int pagebase = a.tab_pagebase[i];
+    // ---------------------------------------------------------------- table metadata
     const int B = s.B;
-    int32_t* page_ids = reinterpret_cast<int32_t*>(hist[0]);  // hist is free after select
-    const int pg_first = surv_base / B;
-    const int pg_count = kept_me > 0 ? (surv_base + kept_me - 1) / B - pg_first + 1 : 0;
-    for (int p = tid; p < pg_count && p < 512; p += nthr)
-        page_ids[p] = s.stack[pop_base - 1 - (pagebase + pg_first + p)];
-    __syncthreads();
-    const bool ids_cached = pg_count <= 512;
-    for (int m0 = wid * 16; m0 < kept_me; m0 += nw * 16) {
-        const int m = m0 + (lane >> 1);
-        const bool valid = m < kept_me;
-        const int jl = valid ? list[m] : 0;
-        const int q = surv_base + m;
-        const int pidx = q / B - pg_first;
-        const int page = valid ? (ids_cached ? page_ids[pidx] : s.stack[pop_base - 1 - (pagebase + q / B)]) : 0;
-        const int slot = q % B;
-        const uint8_t* ks = kbase + (int64_t)(lo + jl) * a.token_stride;
-        const uint8_t* vs = vbase + (int64_t)(lo + jl) * a.token_stride;
-        uint8_t* kd = s.pages + (((int64_t)page * 2 + 0) * B + slot) * s.pitch;
-        uint8_t* vd = s.pages + (((int64_t)page * 2 + 1) * B + slot) * s.pitch;
-        if (valid) {
-            const int qq = lane & 1;
-            if ((s.row_bytes & 63) == 0) {
-                for (int off = qq * 32; off < s.row_bytes; off += 64) stg256(kd + off, ldg256(ks + off));
-                for (int off = qq * 32; off < s.row_bytes; off += 64) stg256(vd + off, ldg256(vs + off));
-            } else {
-                for (int off = qq * 16; off < s.row_bytes; off += 32)
-                    *reinterpret_cast<uint4*>(kd + off) = __ldcs(reinterpret_cast<const uint4*>(ks + off));
-                for (int off = qq * 16; off < s.row_bytes; off += 32)
-                    *reinterpret_cast<uint4*>(vd + off) = __ldcs(reinterpret_cast<const uint4*>(vs + off));
-            }
-            if (qq == 0) {
-                s.positions[(int64_t)page * B + slot] = lo + jl;
-                s.token_scores[(int64_t)page * B + slot] = __longlong_as_double(static_cast<long long>(keys[jl]));
-            }
-        }
-    }
     const int n_pages = (keep + B - 1) / B;
     if (r == 0) {
+        const int pop_base = ctl->pop_base;
+        const int pagebase = a.tab_pagebase[i];
         for (int p = tid; p < n_pages; p += nthr) {
             s.block_table[(int64_t)t * s.max_pages + p] = s.stack[pop_base - 1 - (pagebase + p)];
         }
@@ -343,19 +302,71 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackT
             if (a.evicted_counts) a.evicted_counts[i] = E;
         }
     }
-
-    // ---------------------------------------------------------------- 5. page scores
-    __threadfence();
+    // no CTA may leave while cluster peers can still read its shared memory
     cluster.sync();
-    const int full_pages = keep / B;
-    for (int p = tid; p < full_pages; p += nthr) {
-        const int qlast = p * B + B - 1;
-        if (qlast < surv_base || qlast >= surv_base + kept_me) continue;
-        const int page = s.stack[pop_base - 1 - (pagebase + p)];
-        double sum = 0.0;
-        for (int j = 0; j < B; ++j) sum += __ldcg(s.token_scores + (int64_t)page * B + j);
-        s.page_scores[page] = sum / static_cast<double>(B);
+    (void)kept_me;
+    (void)lane;
+    (void)wid;
+    (void)nw;
+}
+
+// ---------------------------------------------------------------------------
+// prefill_copy_kernel: one warp per destination page. Lane pair r moves the
+// page's slot r: survivor q = page*B + r (position order) -> K and V rows
+// with 256-bit loads/stores, position and cached score beside the page; the
+// warp then sums the B scores in slot order (page_score, importance.cpp:19-30)
+// for a full page. Grid (ceil(max pages / 4), n_tab).
+__global__ void __launch_bounds__(128) prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
+    if (ctl->abort) return;
+    const int i = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int j = blockIdx.x * (blockDim.x >> 5) + wid;
+    const int L = a.tab_len[i];
+    const int keep = (s.policy == PE_POLICY_PAGED_EVICTION && L > s.C) ? s.C : L;
+    const int B = s.B;
+    const int n_pages = (keep + B - 1) / B;
+    if (j >= n_pages) return;
+    const int h = i % s.tab_heads;
+    const int64_t row0 = (a.tab_tok0[i] * s.tab_heads + h) * (int64_t)s.row_bytes;
+    const uint8_t* kbase = a.k + row0;
+    const uint8_t* vbase = a.v + row0;
+    const int pagebase = a.tab_pagebase[i];
+    const int page = s.stack[ctl->pop_base - 1 - (pagebase + j)];
+    const int32_t* surv = a.surv + (int64_t)pagebase * B;
+    const unsigned long long* keys = a.keys + a.tab_keybase[i];
+    const int qq = lane & 1;
+    double sum = 0.0;
+    for (int s0 = 0; s0 < B; s0 += 16) {
+        const int slot = s0 + (lane >> 1);
+        const int q = j * B + slot;
+        const bool valid = slot < B && q < keep;
+        const int tok = valid ? __ldg(surv + q) : 0;
+        double S = 0.0;
+        if (valid) {
+            const uint8_t* ks = kbase + (int64_t)tok * a.token_stride;
+            const uint8_t* vs = vbase + (int64_t)tok * a.token_stride;
+            uint8_t* kd = s.pages + (((int64_t)page * 2 + 0) * B + slot) * s.pitch;
+            uint8_t* vd = s.pages + (((int64_t)page * 2 + 1) * B + slot) * s.pitch;
+            if ((s.row_bytes & 63) == 0) {
+                for (int off = qq * 32; off < s.row_bytes; off += 64) stg256(kd + off, ldg256(ks + off));
+                for (int off = qq * 32; off < s.row_bytes; off += 64) stg256(vd + off, ldg256(vs + off));
+            } else {
+                for (int off = qq * 16; off < s.row_bytes; off += 32)
+                    *reinterpret_cast<uint4*>(kd + off) = __ldcs(reinterpret_cast<const uint4*>(ks + off));
+                for (int off = qq * 16; off < s.row_bytes; off += 32)
+                    *reinterpret_cast<uint4*>(vd + off) = __ldcs(reinterpret_cast<const uint4*>(vs + off));
+            }
+            S = __longlong_as_double(static_cast<long long>(__ldg(keys + tok)));
+            if (qq == 0) {
+                s.positions[(int64_t)page * B + slot] = tok;
+                s.token_scores[(int64_t)page * B + slot] = S;
+            }
+        }
+        const int ns = min(16, B - s0);
+        for (int u = 0; u < ns; ++u) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * u);
     }
+    if (lane == 0 && (j + 1) * B <= keep) s.page_scores[page] = sum / static_cast<double>(B);
 }
 
 }  // namespace pe

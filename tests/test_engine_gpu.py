@@ -264,3 +264,30 @@ def test_cfg1_full_parity():
         pos += 1
     eng.sync()
     check(eng, orc, "cfg1 decode: ")
+
+
+def test_decode_pool_exhaustion_matches_serial_semantics():
+    """A decode append that runs out of pages behaves like the reference's
+    serial loop of append_token calls: tables before the first failing pop
+    (ascending table id) are appended, the failing one and all later ones are
+    not, and PoolExhausted is reported (page_pool.cpp:26-28)."""
+    rng = np.random.default_rng(12)
+    B, C, d, H, S = 4, 8, 8, 1, 6
+    lens = np.array([8, 7, 8, 3, 8, 8])  # tables 0, 2, 4, 5 will need a page on the next append
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    need = int(sum((L + B - 1) // B for L in lens))
+    eng, orc = make_pair(n_seqs=S, n_layers=1, H=H, d=d, B=B, C=C, dtype=oracle.F32, cap=need + 2)
+    k, _ = random_kv(rng, (cu[-1], H, d), oracle.F32)
+    v, _ = random_kv(rng, (cu[-1], H, d), oracle.F32)
+    eng.prefill_compress(0, dev(k), dev(v), cu)
+    orc.prefill(0, k, v, cu)
+    eng.sync()
+    kk, _ = random_kv(rng, (1, S, H, d), oracle.F32)
+    vv, _ = random_kv(rng, (1, S, H, d), oracle.F32)
+    pos = lens.astype(np.int64)
+    eng.append_token(0, 1, dev(kk), dev(vv), dev(pos))
+    with pytest.raises(pe.PoolExhausted):
+        eng.sync()
+    assert orc.decode_append(0, 1, kk, vv, pos) == 2
+    check(eng, orc, "exhaustion: ")
+    assert list(eng.tables()[3]) == [9, 8, 9, 4, 8, 8]  # tables 0..3 appended, 4 failed, 5 stopped
