@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -79,13 +80,19 @@ struct pe_engine {
     int32_t* h_tab_len = nullptr;       // pinned
     int64_t* h_tab_tok0 = nullptr;      // pinned
     int32_t* h_tab_pagebase = nullptr;  // pinned
-    // staging for host buffers
-    uint8_t* stage_a = nullptr;
-    size_t stage_a_bytes = 0;
-    uint8_t* stage_b = nullptr;
-    size_t stage_b_bytes = 0;
-    uint8_t* stage_c = nullptr;
-    size_t stage_c_bytes = 0;
+    // staging ring for host buffers: H2D copies run on copy_stream, overlapping
+    // the engine's kernels; slot reuse is guarded by "consumed" events
+    static constexpr int kRing = 8;
+    struct Slot {
+        uint8_t* buf = nullptr;
+        size_t bytes = 0;
+        cudaEvent_t ready = nullptr;     // copy done (copy_stream)
+        cudaEvent_t consumed = nullptr;  // last reader done (compute stream)
+    } ring[kRing];
+    int ring_next = 0;
+    int pending[4];                      // slots staged by the current call
+    int n_pending = 0;
+    cudaStream_t copy_stream = nullptr;
     float* part_o = nullptr;
     size_t part_o_elems = 0;
     float* part_ml = nullptr;
@@ -97,16 +104,6 @@ struct pe_engine {
 };
 
 namespace {
-
-pe_status ensure(uint8_t** buf, size_t* have, size_t need) {
-    if (*have >= need) return PE_OK;
-    if (*buf) cudaFree(*buf);
-    *buf = nullptr;
-    *have = 0;
-    PE_CUDA(cudaMalloc(buf, need));
-    *have = need;
-    return PE_OK;
-}
 
 template <typename T>
 pe_status ensure_t(T** buf, size_t* have, size_t need) {
@@ -120,20 +117,39 @@ pe_status ensure_t(T** buf, size_t* have, size_t need) {
 }
 
 // Device view of an input buffer: device pointers pass through; host
-// buffers are copied into engine staging on `st`.
-pe_status as_device(pe_engine* e, const void* p, size_t bytes, uint8_t** stage, size_t* have,
-                    cudaStream_t st, const uint8_t** out) {
+// buffers are copied into the next staging-ring slot on the engine's copy
+// stream (so the H2D transfer overlaps kernels already queued on `st`), and
+// `st` waits for that copy. mark_consumed() after the call's launches
+// releases the slots.
+pe_status as_device(pe_engine* e, const void* p, size_t bytes, cudaStream_t st, const uint8_t** out) {
     if (p == nullptr) return fail(PE_INVALID_ARG, "null buffer");
     if (is_device_ptr(p)) {
         *out = static_cast<const uint8_t*>(p);
         return PE_OK;
     }
-    pe_status r = ensure(stage, have, bytes);
-    if (r != PE_OK) return r;
-    PE_CUDA(cudaMemcpyAsync(*stage, p, bytes, cudaMemcpyHostToDevice, st));
-    *out = *stage;
-    (void)e;
+    const int k = e->ring_next;
+    e->ring_next = (e->ring_next + 1) % pe_engine::kRing;
+    pe_engine::Slot& sl = e->ring[k];
+    if (sl.bytes < bytes) {
+        PE_CUDA(cudaEventSynchronize(sl.consumed));
+        if (sl.buf) PE_CUDA(cudaFree(sl.buf));
+        sl.buf = nullptr;
+        sl.bytes = 0;
+        PE_CUDA(cudaMalloc(&sl.buf, bytes));
+        sl.bytes = bytes;
+    }
+    PE_CUDA(cudaStreamWaitEvent(e->copy_stream, sl.consumed, 0));
+    PE_CUDA(cudaMemcpyAsync(sl.buf, p, bytes, cudaMemcpyHostToDevice, e->copy_stream));
+    PE_CUDA(cudaEventRecord(sl.ready, e->copy_stream));
+    PE_CUDA(cudaStreamWaitEvent(st, sl.ready, 0));
+    if (e->n_pending < 4) e->pending[e->n_pending++] = k;
+    *out = sl.buf;
     return PE_OK;
+}
+
+void mark_consumed(pe_engine* e, cudaStream_t st) {
+    for (int i = 0; i < e->n_pending; ++i) cudaEventRecord(e->ring[e->pending[i]].consumed, st);
+    e->n_pending = 0;
 }
 
 int32_t elt_size(int32_t dtype) { return dtype == PE_DTYPE_BF16 ? 2 : 4; }
@@ -305,6 +321,17 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             return cleanup_fail(fail(PE_CUDA_ERROR, "state initialisation failed"));
         }
     }
+    if (cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        return cleanup_fail(fail(PE_CUDA_ERROR, "copy stream creation failed"));
+    }
+    for (auto& sl : e->ring) {
+        if (cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            return cleanup_fail(fail(PE_CUDA_ERROR, "event creation failed"));
+        }
+    }
     // kernel attributes: allow dynamic smem up to the opt-in limit minus the static part
     {
         int optin = 0;
@@ -315,10 +342,11 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             *out = optin - static_cast<int>(fa.sharedSizeBytes);
             return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, *out) == cudaSuccess;
         };
-        int mma64 = 0, mma128 = 0;
+        int mma64 = 0, mma128 = 0, sel_cta = 0;
         if (!allow(reinterpret_cast<const void*>(prefill_select_kernel), &e->max_dyn_prefill) ||
             !allow(reinterpret_cast<const void*>(attention_split_kernel), &e->max_dyn_attn) ||
-            !allow(attention_mma_fn(64), &mma64) || !allow(attention_mma_fn(128), &mma128)) {
+            !allow(attention_mma_fn(64), &mma64) || !allow(attention_mma_fn(128), &mma128) ||
+            !allow(reinterpret_cast<const void*>(prefill_select_cta_kernel), &sel_cta)) {
             cudaGetLastError();
             return cleanup_fail(fail(PE_CUDA_ERROR, "cudaFuncSetAttribute(max dynamic smem) failed"));
         }
@@ -336,11 +364,17 @@ pe_status pe_engine_destroy(pe_engine* e) {
                    s.newest_fill, s.retained, s.stack, s.top, s.status, s.evict_count, s.grid_ctr, e->vpage,
                    e->ctl, e->rank,
                    e->work, e->victims, e->tickets, e->evict_scratch, e->tab_len, e->tab_tok0,
-                   e->tab_pagebase, e->evicted_dev, e->stage_a, e->stage_b, e->stage_c, e->part_o,
+                   e->tab_pagebase, e->evicted_dev, e->part_o,
                    e->part_ml, e->out_stage, e->tab_keybase, e->keys, e->surv, e->lb_status};
     for (void* p : dev) {
         if (p) cudaFree(p);
     }
+    for (auto& sl : e->ring) {
+        if (sl.buf) cudaFree(sl.buf);
+        if (sl.ready) cudaEventDestroy(sl.ready);
+        if (sl.consumed) cudaEventDestroy(sl.consumed);
+    }
+    if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
     if (e->h_tab_len) cudaFreeHost(e->h_tab_len);
     if (e->h_tab_tok0) cudaFreeHost(e->h_tab_tok0);
     if (e->h_tab_pagebase) cudaFreeHost(e->h_tab_pagebase);
@@ -387,16 +421,18 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
         }
     }
     const int chunk_cap = (max_len + kPrefillCluster - 1) / kPrefillCluster;
-    const size_t pack_smem = (size_t)chunk_cap * 8;
+    const size_t pack_smem = (size_t)chunk_cap * 12 + 16;  // keys + two u16 candidate lists
+    if (chunk_cap > 65535) return fail(PE_INVALID_ARG, "prefill length exceeds the select kernel's index range");
     if (pack_smem > (size_t)e->max_dyn_prefill)
         return fail(PE_INVALID_ARG, "prefill length " + std::to_string(max_len) +
                                         " exceeds the per-cluster shared-memory capacity");
     const size_t tokens = cu_seqlens[n_seqs];
     const size_t in_bytes = tokens * (size_t)H * s.row_bytes;
     const uint8_t *dk = nullptr, *dv = nullptr;
-    pe_status r = as_device(e, k, in_bytes, &e->stage_a, &e->stage_a_bytes, st, &dk);
+    e->n_pending = 0;
+    pe_status r = as_device(e, k, in_bytes, st, &dk);
     if (r != PE_OK) return r;
-    r = as_device(e, v, in_bytes, &e->stage_b, &e->stage_b_bytes, st, &dv);
+    r = as_device(e, v, in_bytes, st, &dv);
     if (r != PE_OK) return r;
     r = ensure_t(&e->keys, &e->keys_elems, (size_t)total_keys);
     if (r != PE_OK) return r;
@@ -421,14 +457,25 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     a.n_tab = n_tab;
     a.seq_begin = seq_begin;
     a.layer = layer;
-    a.chunk_cap = chunk_cap;
+    // PE_SELECT=cluster forces the cluster kernel (tests exercise both paths)
+    const char* sel_env = std::getenv("PE_SELECT");
+    const bool force_cluster = sel_env != nullptr && std::strcmp(sel_env, "cluster") == 0;
+    const bool use_cta_select = max_len <= kSelectCtaMaxLen && !force_cluster;
+    a.chunk_cap = use_cta_select ? max_len : chunk_cap;  // keys held in smem per CTA
     if (total_pages > INT32_MAX) return fail(PE_POOL_EXHAUSTED, "page pool exhausted");
     plan_prefill_kernel<<<1, 1024, 0, st>>>(s, a, static_cast<int32_t>(total_pages), e->ctl);
     launch_prefill_score_any(e->variant, dim3((max_len + kScoreTokensPerCta - 1) / kScoreTokensPerCta, n_seqs), st, s,
                              a, e->ctl);
-    prefill_select_kernel<<<dim3(kPrefillCluster, n_tab), kPackThreads, pack_smem, st>>>(s, a, e->ctl);
+    if (use_cta_select) {
+        // one CTA per table, high key words in shared memory (no cluster barriers)
+        const size_t sel_smem = (((size_t)max_len * 4 + 15) & ~size_t(15)) + kSelHistCopies * 2048 * 4;
+        prefill_select_cta_kernel<<<n_tab, 1024, sel_smem, st>>>(s, a, e->ctl);
+    } else {
+        prefill_select_kernel<<<dim3(kPrefillCluster, n_tab), kPackThreads, pack_smem, st>>>(s, a, e->ctl);
+    }
     const int max_keep_pages = (std::min(max_len, s.policy == PE_POLICY_PAGED_EVICTION ? s.C : max_len) + s.B - 1) / s.B;
     prefill_copy_kernel<<<dim3((max_keep_pages + 3) / 4, n_tab), 128, 0, st>>>(s, a, e->ctl);
+    mark_consumed(e, st);
     r = check_launch(e, "prefill_kernel");
     if (r != PE_OK) return r;
     e->stats.kernel_launches += 4;
@@ -453,11 +500,12 @@ pe_status pe_decode_append(pe_engine* e, int32_t layer_begin, int32_t n_layers, 
     const int n = ts.size(s);
     const size_t bytes = (size_t)n * s.row_bytes;
     const uint8_t *dk = nullptr, *dv = nullptr, *dp = nullptr;
-    pe_status r = as_device(e, k_rows, bytes, &e->stage_a, &e->stage_a_bytes, st, &dk);
+    e->n_pending = 0;
+    pe_status r = as_device(e, k_rows, bytes, st, &dk);
     if (r != PE_OK) return r;
-    r = as_device(e, v_rows, bytes, &e->stage_b, &e->stage_b_bytes, st, &dv);
+    r = as_device(e, v_rows, bytes, st, &dv);
     if (r != PE_OK) return r;
-    r = as_device(e, positions, sizeof(int64_t) * s.n_seqs, &e->stage_c, &e->stage_c_bytes, st, &dp);
+    r = as_device(e, positions, sizeof(int64_t) * s.n_seqs, st, &dp);
     if (r != PE_OK) return r;
     // one launch: canonical pop ranks by a single-pass decoupled look-back
     const int warps = kAppendThreads / 32;
@@ -467,6 +515,7 @@ pe_status pe_decode_append(pe_engine* e, int32_t layer_begin, int32_t n_layers, 
     e->append_epoch = (e->append_epoch % 0x3FFFFFFF) + 1;
     launch_append_any(e->variant, blocks, st, s, ts, dk, dv, reinterpret_cast<const int64_t*>(dp), e->lb_status,
                       e->ctl, ticket_base, e->append_epoch);
+    mark_consumed(e, st);
     r = check_launch(e, "append_kernel");
     if (r != PE_OK) return r;
     e->stats.kernel_launches += 1;
@@ -538,8 +587,8 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int n_tab = s.n_seqs * s.tab_heads;
     const uint8_t* dq = nullptr;
-    pe_status r = as_device(e, q, (size_t)s.n_seqs * n_q_heads * s.row_bytes, &e->stage_a,
-                            &e->stage_a_bytes, st, &dq);
+    e->n_pending = 0;
+    pe_status r = as_device(e, q, (size_t)s.n_seqs * n_q_heads * s.row_bytes, st, &dq);
     if (r != PE_OK) return r;
     int splits = std::max(1, (e->sm_count * 8 + n_tab - 1) / n_tab);
     splits = std::min(splits, std::max(1, (s.max_pages + 3) / 4));
@@ -579,6 +628,7 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
         attention_split_kernel<<<dim3(splits, n_tab), 128, smem, st>>>(s, a);
     }
     attention_merge_kernel<<<n_tab, 128, 0, st>>>(s, a);
+    mark_consumed(e, st);
     r = check_launch(e, "attention");
     if (r != PE_OK) return r;
     e->stats.kernel_launches += 2;

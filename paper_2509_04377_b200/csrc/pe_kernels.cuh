@@ -34,6 +34,9 @@ __global__ void evict_cached_kernel(DevState s, TableSet ts, double* scratch, in
                                     unsigned long long grid_last);
 __global__ void plan_prefill_kernel(DevState s, PrefillArgs a, int32_t total_pages, LaunchCtl* ctl);
 __global__ void prefill_select_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
+__global__ void prefill_select_cta_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
+constexpr int kSelHistCopies = 8;        // private histogram copies in the CTA select kernel
+constexpr int kSelectCtaMaxLen = 36864;  // CTA-per-table select: 4 B of smem per token + 64 KB histograms
 __global__ void prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 
 // host-side launchers of the row-geometry-specialised kernels (pe_score.cuh variants)

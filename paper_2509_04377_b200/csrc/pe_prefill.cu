@@ -15,8 +15,10 @@
 //               is the double order), 8 B per token to a key buffer.
 //  select/compact run in prefill_select_kernel, one cluster of 8 CTAs per
 //  table, CTA r owning tokens [L*r/8, L*(r+1)/8) whose keys it loads to smem:
-//  2. select  — cluster-wide MSB radix select (8-bit digits, histograms merged
-//               through DSMEM) of the E-th smallest key: every key with a
+//  2. select  — cluster-wide MSB radix select (8-bit digits after the common
+//               prefix of the cluster min/max, candidate lists compacted each
+//               pass, histograms merged through DSMEM) of the E-th smallest
+//               key: every key with a
 //               smaller prefix is evicted; among keys equal to the final
 //               prefix, the first k_rem in position order (the reference's
 //               position tie rule).
@@ -111,6 +113,76 @@ void launch_prefill_score_any(int variant, dim3 grid, cudaStream_t st, const Dev
     PE_SCORE_DISPATCH(variant, (launch_score<SV>(grid, st, s, a, ctl)));
 }
 
+// Warp-interleaved position-order sweeps over n positions (conflict-free
+// shared-memory access): warp w owns positions [w*span, (w+1)*span), visited
+// in rounds of 32 consecutive positions (lane = position % 32); ranks come
+// from ballots, so the order is exactly ascending position.
+__device__ __forceinline__ int sweep_span(int n) {
+    const int nw = blockDim.x >> 5;
+    return ((n + nw * 32 - 1) / (nw * 32)) * 32;
+}
+
+template <typename F>
+__device__ __forceinline__ void sweep_count(int n, F classify, int* warp_less, int* warp_tie) {
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int span = sweep_span(n);
+    const int end = min(n, (wid + 1) * span);
+    int lc = 0, tc = 0;
+    for (int base = wid * span; base < end; base += 32) {
+        const int p = base + lane;
+        bool l = false, t = false;
+        if (p < end) classify(p, l, t);
+        lc += __popc(__ballot_sync(0xFFFFFFFFu, l));
+        tc += __popc(__ballot_sync(0xFFFFFFFFu, t));
+    }
+    if (lane == 0) {
+        warp_less[wid] = lc;
+        warp_tie[wid] = tc;
+    }
+}
+
+// Turns per-warp (less, tie) counts into per-warp tie / survivor bases (one
+// thread), given the CTA's first tie rank and first survivor index.
+__device__ __forceinline__ void sweep_bases(int n, int k_rem, int tie0, int surv0, const int* warp_less,
+                                            const int* warp_tie, int* tie_base, int* keep_base) {
+    const int nw = blockDim.x >> 5;
+    const int span = sweep_span(n);
+    int tb = tie0, kb = surv0;
+    for (int w = 0; w < nw; ++w) {
+        const int nwn = max(0, min(n, (w + 1) * span) - w * span);
+        tie_base[w] = tb;
+        keep_base[w] = kb;
+        const int ev = max(0, min(k_rem - tb, warp_tie[w]));
+        kb += nwn - warp_less[w] - ev;
+        tb += warp_tie[w];
+    }
+}
+
+template <typename F, typename EMIT>
+__device__ __forceinline__ void sweep_emit(int n, F classify, int k_rem, const int* tie_base, const int* keep_base,
+                                           EMIT emit) {
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int span = sweep_span(n);
+    const int end = min(n, (wid + 1) * span);
+    const unsigned lt = (1u << lane) - 1u;
+    int tie_run = tie_base[wid];
+    int keep_run = keep_base[wid];
+    for (int base = wid * span; base < end; base += 32) {
+        const int p = base + lane;
+        bool l = false, t = false;
+        if (p < end) classify(p, l, t);
+        const unsigned tb = __ballot_sync(0xFFFFFFFFu, t);
+        const bool evict = l || (t && tie_run + __popc(tb & lt) < k_rem);
+        tie_run += __popc(tb);
+        const bool keep = p < end && !evict;
+        const unsigned kb = __ballot_sync(0xFFFFFFFFu, keep);
+        if (keep) emit(keep_run + __popc(kb & lt), p);
+        keep_run += __popc(kb);
+    }
+}
+
 // Warp-aggregated shared-memory histogram increment (many keys share a
 // digit: S values of one table are concentrated).
 __device__ __forceinline__ void hist_add(uint32_t* hb, uint32_t bin, bool active) {
@@ -126,7 +198,6 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackT
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t hist[2][256];
     __shared__ uint32_t tot[256];
-    __shared__ int scan_sm[33];
     __shared__ int xchg[2];
     __shared__ int bc[8];
 
@@ -151,40 +222,103 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackT
     const int t = (seq * s.n_layers + a.layer) * s.tab_heads + h;
 
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
+    // candidate index lists (double-buffered) for the radix passes
+    uint16_t* cand[2] = {reinterpret_cast<uint16_t*>(smem + (size_t)a.chunk_cap * 8),
+                         reinterpret_cast<uint16_t*>(smem + (size_t)a.chunk_cap * 10)};
+    __shared__ unsigned long long mm[2];
+    __shared__ int cand_n[2];
+    __shared__ uint32_t wh[8 * 256];  // per-warp histogram copies (reduced into hb)
     // survivor q of table i (position order) -> its token index
     int32_t* surv = a.surv + (int64_t)a.tab_pagebase[i] * s.B;
 
-    // ---------------------------------------------------------------- 1. keys -> smem
+    // ---------------------------------------------------------------- 1. keys -> smem (+ min/max)
+    unsigned long long kmin = ~0ull, kmax = 0ull;
     {
         const unsigned long long* g = a.keys + a.tab_keybase[i] + lo;
-        for (int j = tid; j < n; j += nthr) keys[j] = __ldcs(g + j);
+        for (int j0 = tid; j0 < n; j0 += 8 * nthr) {  // 8 independent loads in flight per thread
+            unsigned long long kv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) kv[u] = (j0 + u * nthr < n) ? __ldcs(g + j0 + u * nthr) : 0ull;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (j0 + u * nthr < n) {
+                    keys[j0 + u * nthr] = kv[u];
+                    kmin = min(kmin, kv[u]);
+                    kmax = max(kmax, kv[u]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xFFFFFFFFu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xFFFFFFFFu, kmax, o));
+    }
+    if (tid == 0) {
+        mm[0] = ~0ull;
+        mm[1] = 0ull;
+    }
+    __syncthreads();
+    if (lane == 0) {
+        atomicMin(&mm[0], kmin);
+        atomicMax(&mm[1], kmax);
     }
     __syncthreads();
 
     // ---------------------------------------------------------------- 2. select
+    // MSB radix select of the E-th smallest key. All keys share the common
+    // prefix of the cluster-wide (min, max), so the passes start right after
+    // it; each pass histograms only the candidates still matching the prefix
+    // (compacted index lists), merged across the cluster through DSMEM.
     int k_rem = 0;
     int final_shift = 64;
     unsigned long long prefix = 0;
     if (E > 0) {
         k_rem = E;
-        int shift = 64;
-        for (int pass = 0; pass < 8; ++pass) {
-            shift -= 8;
+        cluster.sync();
+        unsigned long long gmin = ~0ull, gmax = 0ull;
+        for (int rr = 0; rr < CL; ++rr) {
+            const unsigned long long* rm = cluster.map_shared_rank(mm, rr);
+            gmin = min(gmin, rm[0]);
+            gmax = max(gmax, rm[1]);
+        }
+        const int cpl = (gmin == gmax) ? 64 : __clzll(gmin ^ gmax);
+        int bitpos = 64 - cpl;  // unresolved low bits
+        prefix = cpl == 0 ? 0ull : (cpl == 64 ? gmin : (gmin >> bitpos));
+        final_shift = bitpos;
+        int pass = 0;
+        while (bitpos > 0) {
+            const int bits = min(8, bitpos);
+            const int shift = bitpos - bits;
+            const unsigned long long dmask = (1ull << bits) - 1ull;
             uint32_t* hb = hist[pass & 1];
-            for (int b = tid; b < 256; b += nthr) hb[b] = 0;
+            uint16_t* out = cand[pass & 1];
+            const uint16_t* in = cand[(pass & 1) ^ 1];
+            const int n_in = pass == 0 ? n : cand_n[(pass & 1) ^ 1];
+            for (int b = tid; b < 8 * 256; b += nthr) wh[b] = 0;
             __syncthreads();
-            const int n_round = (n + nthr - 1) / nthr * nthr;
-            for (int j = tid; j < n_round; j += nthr) {
-                const unsigned long long key = j < n ? keys[j] : 0ull;
-                const bool match = j < n && ((pass == 0) || ((key >> (shift + 8)) == prefix));
-                hist_add(hb, static_cast<uint32_t>((key >> shift) & 255u), match);
+            const int n_round = (n_in + nthr - 1) / nthr * nthr;
+            for (int x = tid; x < n_round; x += nthr) {
+                const bool act = x < n_in;
+                const int j = act ? (pass == 0 ? x : in[x]) : 0;
+                const unsigned long long key = act ? keys[j] : 0ull;
+                hist_add(wh + (wid & 7) * 256, static_cast<uint32_t>((key >> shift) & dmask), act);
+            }
+            __syncthreads();
+            for (int b = tid; b < 256; b += nthr) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc += wh[c * 256 + b];
+                hb[b] = acc;
             }
             cluster.sync();
             for (int b = tid; b < 256; b += nthr) {
                 uint32_t acc = 0;
-                for (int rr = 0; rr < CL; ++rr) acc += cluster.map_shared_rank(hb, rr)[b];
+#pragma unroll
+                for (int rr = 0; rr < kPrefillCluster; ++rr) acc += cluster.map_shared_rank(hb, rr)[b];
                 tot[b] = acc;
             }
+            if (tid == 0) cand_n[pass & 1] = 0;
             __syncthreads();
             if (wid == 0) {
                 uint32_t part[8];
@@ -208,41 +342,48 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackT
             __syncthreads();
             const int d = bc[0];
             k_rem -= bc[1];
-            prefix = (prefix << 8) | static_cast<unsigned long long>(d);
+            prefix = (prefix << bits) | static_cast<unsigned long long>(d);
             final_shift = shift;
-            const bool done = static_cast<int>(tot[d]) == k_rem;
+            bitpos = shift;
+            if (static_cast<int>(tot[d]) == k_rem || bitpos == 0) break;
+            // compact the candidates that carry the chosen digit
+            for (int x = tid; x < n_round; x += nthr) {
+                const bool act = x < n_in;
+                const int j = act ? (pass == 0 ? x : in[x]) : 0;
+                const bool keep_c = act && static_cast<int>((keys[j] >> shift) & dmask) == d;
+                const unsigned bal = __ballot_sync(0xFFFFFFFFu, keep_c);
+                int base = 0;
+                if (lane == 0 && bal) base = atomicAdd(&cand_n[pass & 1], __popc(bal));
+                base = __shfl_sync(0xFFFFFFFFu, base, 0);
+                if (keep_c) out[base + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint16_t>(j);
+            }
             __syncthreads();
-            if (done) break;
+            ++pass;
         }
     }
 
     // ---------------------------------------------------------------- 3. compact
-    auto classify = [&](unsigned long long key, bool& less, bool& tie) {
+    __shared__ int w_less[32], w_tie[32], w_tieb[32], w_keepb[32];
+    auto classify = [&](int j, bool& less, bool& tie) {
         if (E == 0) {
             less = false;
             tie = false;
             return;
         }
-        const unsigned long long top = key >> final_shift;
+        const unsigned long long top = keys[j] >> final_shift;
         less = top < prefix;
         tie = top == prefix;
     };
-    const int seg = (n + nthr - 1) / nthr;
-    const int a0 = min(n, tid * seg);
-    const int a1 = min(n, a0 + seg);
-    int less_t = 0, tie_t = 0;
-    for (int j = a0; j < a1; ++j) {
-        bool l, tt;
-        classify(keys[j], l, tt);
-        less_t += l;
-        tie_t += tt;
-    }
-    int less_cta, tie_cta;
-    block_excl_scan(less_t, scan_sm, &less_cta);
-    const int tie_before = block_excl_scan(tie_t, scan_sm, &tie_cta);
+    sweep_count(n, classify, w_less, w_tie);
+    __syncthreads();
     if (tid == 0) {
-        xchg[0] = less_cta;
-        xchg[1] = tie_cta;
+        int lc = 0, tc = 0;
+        for (int w = 0; w < nw; ++w) {
+            lc += w_less[w];
+            tc += w_tie[w];
+        }
+        xchg[0] = lc;
+        xchg[1] = tc;
     }
     cluster.sync();
     if (tid == 0) {
@@ -261,29 +402,12 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackT
             if (rr == r) kept_me = kept;
             tb += t_rr;
         }
-        bc[2] = tie_base;
-        bc[3] = surv_base;
         bc[4] = kept_me;
+        sweep_bases(n, k_rem, tie_base, surv_base, w_less, w_tie, w_tieb, w_keepb);
     }
     __syncthreads();
-    const int tie_base = bc[2];
-    const int surv_base = bc[3];
     const int kept_me = bc[4];
-    const int my_tie0 = tie_base + tie_before;
-    const int ev_ties_t = max(0, min(k_rem - my_tie0, tie_t));
-    const int keep_t = (a1 - a0) - less_t - ev_ties_t;
-    int keep_cta;
-    int q_local = block_excl_scan(keep_t, scan_sm, &keep_cta);
-    {
-        int tr = my_tie0;
-        for (int j = a0; j < a1; ++j) {
-            bool l, tt;
-            classify(keys[j], l, tt);
-            const bool evict = l || (tt && tr < k_rem);
-            tr += tt;
-            if (!evict) surv[surv_base + q_local++] = lo + j;
-        }
-    }
+    sweep_emit(n, classify, k_rem, w_tieb, w_keepb, [&](int q, int j) { surv[q] = lo + j; });
     __syncthreads();
 
     // ---------------------------------------------------------------- table metadata
@@ -308,6 +432,222 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackT
     (void)lane;
     (void)wid;
     (void)nw;
+}
+
+// ---------------------------------------------------------------------------
+// prefill_select_cta_kernel: the select/compact step for tables of up to
+// kSelectCtaMaxLen tokens with ONE CTA (1024 threads) per table and no
+// cluster barriers. The high 32 bits of every key live in shared memory
+// (the order of the high words is the order of the keys' high halves);
+// radix passes of 11-bit digits after the common prefix of (min, max) run
+// on them with block barriers only. If the boundary high word is shared by
+// several keys, their low words (read from global memory, only for those
+// keys) are resolved with further passes. Then one position-order sweep
+// (block scans) emits the survivors. Same decisions as the cluster kernel.
+__device__ __forceinline__ void reduce_hist_copies(const uint32_t* copies, uint32_t* out, int nbins) {
+    for (int b = threadIdx.x; b < 2048; b += blockDim.x) {
+        uint32_t acc = 0;
+        if (b < nbins) {
+#pragma unroll
+            for (int c = 0; c < kSelHistCopies; ++c) acc += copies[c * 2048 + b];
+        }
+        out[b] = acc;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ int block_find_digit(const uint32_t* hist, int nbins, int k_rem, int* bc, int* scan_sm) {
+    // exclusive scan over bins (2 per thread for 2048 bins / 1024 threads)
+    const int per = (nbins + blockDim.x - 1) / blockDim.x;
+    const int b0 = min(nbins, (int)threadIdx.x * per);
+    const int b1 = min(nbins, b0 + per);
+    int local = 0;
+    for (int b = b0; b < b1; ++b) local += static_cast<int>(hist[b]);
+    int total;
+    int cum = block_excl_scan(local, scan_sm, &total);
+    for (int b = b0; b < b1; ++b) {
+        const int c = static_cast<int>(hist[b]);
+        if (cum < k_rem && k_rem <= cum + c) {
+            bc[0] = b;
+            bc[1] = cum;
+            bc[2] = c;
+        }
+        cum += c;
+    }
+    __syncthreads();
+    return bc[0];
+}
+
+__global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint32_t hist[2048];  // reduced histogram
+    __shared__ int scan_sm[33];
+    __shared__ int bc[4];
+    __shared__ unsigned int mm[2];
+    if (ctl->abort) return;
+    const int i = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    const int L = a.tab_len[i];
+    const int keep = (s.policy == PE_POLICY_PAGED_EVICTION && L > s.C) ? s.C : L;
+    const int E = L - keep;
+    const int h = i % s.tab_heads;
+    const int seq = a.seq_begin + i / s.tab_heads;
+    const int t = (seq * s.n_layers + a.layer) * s.tab_heads + h;
+    const int B = s.B;
+    uint32_t* hi = reinterpret_cast<uint32_t*>(smem);
+    // kSelHistCopies private histograms (warp w -> copy w % kSelHistCopies):
+    // the early digits of a table's keys are concentrated in a few bins, so a
+    // single histogram would serialise every warp's atomics on them
+    uint32_t* hcopy = reinterpret_cast<uint32_t*>(smem + (((size_t)a.chunk_cap * 4 + 15) & ~size_t(15)));
+    uint32_t* my_hist = hcopy + ((threadIdx.x >> 5) % kSelHistCopies) * 2048;
+    const unsigned long long* gk = a.keys + a.tab_keybase[i];
+    int32_t* surv = a.surv + (int64_t)a.tab_pagebase[i] * B;
+
+    // ---- 1. high words -> smem, min/max
+    unsigned int hmin = 0xFFFFFFFFu, hmax = 0u;
+    for (int j0 = tid; j0 < L; j0 += 8 * nthr) {  // 8 independent loads in flight per thread
+        unsigned long long kv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) kv[u] = (j0 + u * nthr < L) ? __ldcs(gk + j0 + u * nthr) : 0ull;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (j0 + u * nthr < L) {
+                const uint32_t w = static_cast<uint32_t>(kv[u] >> 32);
+                hi[j0 + u * nthr] = w;
+                hmin = min(hmin, w);
+                hmax = max(hmax, w);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        hmin = min(hmin, __shfl_xor_sync(0xFFFFFFFFu, hmin, o));
+        hmax = max(hmax, __shfl_xor_sync(0xFFFFFFFFu, hmax, o));
+    }
+    if (tid == 0) {
+        mm[0] = 0xFFFFFFFFu;
+        mm[1] = 0u;
+    }
+    __syncthreads();
+    if ((tid & 31) == 0) {
+        atomicMin(&mm[0], hmin);
+        atomicMax(&mm[1], hmax);
+    }
+    __syncthreads();
+
+    // ---- 2. radix select: threshold key prefix `prefix` of (64 - fshift) bits
+    int k_rem = 0;
+    int fshift = 64;  // 64: nothing evicted (E == 0)
+    unsigned long long prefix = 0;
+    if (E > 0) {
+        k_rem = E;
+        const unsigned int gmin = mm[0], gmax = mm[1];
+        const int cpl = (gmin == gmax) ? 32 : __clz(gmin ^ gmax);
+        int bitpos = 32 - cpl;  // unresolved bits of the high word
+        unsigned int hp = cpl == 0 ? 0u : (cpl == 32 ? gmin : (gmin >> bitpos));
+        fshift = 32 + bitpos;
+        bool done = false;
+        while (bitpos > 0) {  // high-word passes (shared memory)
+            const int bits = min(11, bitpos);
+            const int shift = bitpos - bits;
+            const unsigned int dmask = (1u << bits) - 1u;
+            for (int b = tid; b < kSelHistCopies * 2048; b += nthr) hcopy[b] = 0;
+            __syncthreads();
+            const int n_round = (L + nthr - 1) / nthr * nthr;
+            for (int j = tid; j < n_round; j += nthr) {
+                const unsigned int w = j < L ? hi[j] : 0u;
+                const bool act = j < L && (bitpos == 32 || (w >> bitpos) == hp);
+                hist_add(my_hist, (w >> shift) & dmask, act);
+            }
+            __syncthreads();
+            reduce_hist_copies(hcopy, hist, 1 << bits);
+            const int d = block_find_digit(hist, 1 << bits, k_rem, bc, scan_sm);
+            k_rem -= bc[1];
+            hp = (bitpos == 32 ? 0u : (hp << bits)) | static_cast<unsigned int>(d);
+            bitpos = shift;
+            fshift = 32 + shift;
+            done = bc[2] == k_rem;
+            __syncthreads();
+            if (done) break;
+        }
+        prefix = static_cast<unsigned long long>(hp);
+        if (!done && bitpos == 0) {
+            // the boundary high word is shared: resolve the low words of
+            // those keys only (read from global memory)
+            int lbit = 32;
+            unsigned int lp = 0u;
+            while (lbit > 0) {
+                const int bits = min(11, lbit);
+                const int shift = lbit - bits;
+                const unsigned int dmask = (1u << bits) - 1u;
+                for (int b = tid; b < kSelHistCopies * 2048; b += nthr) hcopy[b] = 0;
+                __syncthreads();
+                const int n_round = (L + nthr - 1) / nthr * nthr;
+                for (int j = tid; j < n_round; j += nthr) {
+                    bool act = j < L && hi[j] == hp;
+                    unsigned int lw = 0u;
+                    if (act) {
+                        lw = static_cast<unsigned int>(__ldcg(gk + j));
+                        act = (lbit == 32) || (lw >> lbit) == lp;
+                    }
+                    hist_add(my_hist, (lw >> shift) & dmask, act);
+                }
+                __syncthreads();
+                reduce_hist_copies(hcopy, hist, 1 << bits);
+                const int d = block_find_digit(hist, 1 << bits, k_rem, bc, scan_sm);
+                k_rem -= bc[1];
+                lp = (lbit == 32 ? 0u : (lp << bits)) | static_cast<unsigned int>(d);
+                lbit = shift;
+                const bool dn = bc[2] == k_rem;
+                __syncthreads();
+                if (dn) break;
+            }
+            fshift = lbit;
+            prefix = (static_cast<unsigned long long>(hp) << (32 - lbit)) | (lp);
+        }
+    }
+
+    // ---- 3. position-order sweep: evict iff key-prefix < prefix, or equal and
+    // among the first k_rem such keys (older first, importance.cpp:46-52)
+    __shared__ int w_less[32], w_tie[32], w_tieb[32], w_keepb[32];
+    auto classify = [&](int j, bool& less, bool& tie) {
+        less = false;
+        tie = false;
+        if (E == 0) return;
+        if (fshift >= 32) {
+            const unsigned long long top = static_cast<unsigned long long>(hi[j]) >> (fshift - 32);
+            less = top < prefix;
+            tie = top == prefix;
+        } else {
+            const unsigned long long hp64 = prefix >> (32 - fshift);
+            const unsigned long long hw = hi[j];
+            if (hw != hp64) {
+                less = hw < hp64;
+            } else {
+                const unsigned long long top = __ldcg(gk + j) >> fshift;
+                less = top < prefix;
+                tie = top == prefix;
+            }
+        }
+    };
+    sweep_count(L, classify, w_less, w_tie);
+    __syncthreads();
+    if (tid == 0) sweep_bases(L, k_rem, 0, 0, w_less, w_tie, w_tieb, w_keepb);
+    __syncthreads();
+    sweep_emit(L, classify, k_rem, w_tieb, w_keepb, [&](int q, int j) { surv[q] = j; });
+    // ---- 4. table metadata
+    const int n_pages = (keep + B - 1) / B;
+    const int pop_base = ctl->pop_base;
+    const int pagebase = a.tab_pagebase[i];
+    for (int p = tid; p < n_pages; p += nthr)
+        s.block_table[(int64_t)t * s.max_pages + p] = s.stack[pop_base - 1 - (pagebase + p)];
+    if (tid == 0) {
+        s.num_pages[t] = n_pages;
+        s.newest_fill[t] = keep - (n_pages - 1) * B;
+        s.retained[t] = keep;
+        if (a.evicted_counts) a.evicted_counts[i] = E;
+    }
 }
 
 // ---------------------------------------------------------------------------

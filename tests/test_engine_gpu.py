@@ -48,9 +48,16 @@ def check(eng, orc, what="", pages=True):
                 assert st["page_scores"][pid] == ost["page_scores"][pid], f"{what}page score {pid}"
 
 
+@pytest.fixture(params=["cta", "cluster"])
+def select_path(request, monkeypatch):
+    """Run prefill through both select kernels (CTA-per-table and cluster)."""
+    monkeypatch.setenv("PE_SELECT", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("dtype", [oracle.F32, oracle.BF16])
 @pytest.mark.parametrize("gen", [random_kv, grid_kv])
-def test_prefill_parity(dtype, gen):
+def test_prefill_parity(dtype, gen, select_path):
     rng = np.random.default_rng(100 + dtype)
     B, C, d, H = 16, 64, 64 if dtype == oracle.F32 else 128, 2
     lens = np.array([C + 1, 3 * C + 7, C, 5, 1, 2 * C, 1000])
@@ -67,7 +74,7 @@ def test_prefill_parity(dtype, gen):
     check(eng, orc, "prefill: ")
 
 
-def test_prefill_ties_across_cta_boundaries():
+def test_prefill_ties_across_cta_boundaries(select_path):
     """Every token of a table scores identically: the E evicted tokens must be
     exactly the oldest E (position tie rule, importance.cpp:46-52), even
     though the ties straddle the 8 CTAs of the cluster."""
@@ -291,3 +298,20 @@ def test_decode_pool_exhaustion_matches_serial_semantics():
     assert orc.decode_append(0, 1, kk, vv, pos) == 2
     check(eng, orc, "exhaustion: ")
     assert list(eng.tables()[3]) == [9, 8, 9, 4, 8, 8]  # tables 0..3 appended, 4 failed, 5 stopped
+
+
+@pytest.mark.slow
+def test_prefill_long_context_cluster_select():
+    """Tables longer than the CTA select limit (49152 tokens) take the
+    cluster select kernel: 2 sequences x 2 KV heads at 60000 tokens."""
+    rng = np.random.default_rng(60000)
+    B, C, d, H = 16, 4096, 128, 2
+    lens = np.array([60000, 50001])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=2, n_layers=1, H=H, d=d, B=B, C=C, dtype=oracle.BF16)
+    k, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+    v, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+    ev = eng.prefill_compress(0, dev(k), dev(v), cu, evicted_counts=True)
+    _, oev = orc.prefill(0, k, v, cu)
+    np.testing.assert_array_equal(ev, oev)
+    check(eng, orc, "long: ")
