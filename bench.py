@@ -112,6 +112,33 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def ncu_traffic(kernel_substr="evict_score_kernel"):
+    """Mean DRAM bytes (read+write) per launch of `kernel_substr` from the
+    committed ncu launch list of this command (profiles/*bench_launches*.csv,
+    `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
+    dram__bytes_write.sum ... python bench.py`), or None."""
+    import csv
+    import glob
+
+    files = sorted(glob.glob(str(ROOT / "profiles" / "*bench_launches*.csv")))
+    if not files:
+        return None
+    rows = list(csv.reader(open(files[-1])))
+    try:
+        h = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    except IndexError:
+        return None
+    hdr = rows[h]
+    ki, mi, vi, ii = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
+    per = {}
+    for r in rows[h + 1:]:
+        if kernel_substr in r[ki] and r[mi].startswith("dram__bytes"):
+            per[r[ii]] = per.get(r[ii], 0.0) + float(r[vi].replace(",", "")) * (
+                1e9 if "Gbyte" in r[hdr.index("Metric Unit")] else 1e6 if "Mbyte" in r[hdr.index("Metric Unit")]
+                else 1.0)
+    return round(sum(per.values()) / len(per)) if per else None
+
+
 # --------------------------------------------------------------------------- helpers
 def k2_bytes_per_table(C, row):
     return (C + B) * row + 8 * (C // B + 1) + 4
@@ -145,14 +172,13 @@ def run_reference(args, cfg, world, rank):
     row_alg = 2 * cfg["d"] * (2 if cfg["dtype"] == "bf16" else 4)
     C = cfg["C"]
     # bounded sample: `tables` tables per step, one eviction cycle each
-    tables = args.ref_tables or max(threads, 64)
-    times = []
-    for it in range(args.warmup + args.steps):
-        secs, ev = ref.bench_decode_cycles(tables, C, B, cfg["d"], threads, 1, seed=it + 1)
-        assert ev == tables, (ev, tables)
-        if it >= args.warmup:
-            times.append(secs)
-    per_step = sum(times) / len(times)
+    tables = args.ref_tables or 1024
+    # one session: W untimed warm-up cycles, then K timed cycles (one step each)
+    secs, ev = ref.bench_decode_cycles(tables, C, B, cfg["d"], threads, args.steps, seed=1,
+                                       warmup_cycles=args.warmup)
+    assert ev == tables * args.steps, (ev, tables)
+    per_step = secs / args.steps
+    times = [per_step]
     bytes_step = tables * (k2_bytes_per_table(C, row_alg) + B * (row_alg + 4))
     value = bytes_step / per_step / 1e9
     line = {
@@ -183,14 +209,18 @@ def cpu_baseline(cfg, args):
         return {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
                 "sample": f"unavailable: {exc}"}
     threads = os.cpu_count() or 1
-    tables = args.ref_tables or max(threads, 64)
+    tables = args.ref_tables or 1024
+    cycles = 4
     row_alg = 2 * cfg["d"] * (2 if cfg["dtype"] == "bf16" else 4)
-    secs, ev = ref.bench_decode_cycles(tables, cfg["C"], B, cfg["d"], threads, 1, seed=7)
-    bytes_step = tables * (k2_bytes_per_table(cfg["C"], row_alg) + B * (row_alg + 4))
+    secs, ev = ref.bench_decode_cycles(tables, cfg["C"], B, cfg["d"], threads, cycles, seed=7,
+                                       warmup_cycles=1)
+    bytes_step = cycles * tables * (k2_bytes_per_table(cfg["C"], row_alg) + B * (row_alg + 4))
     return {"value": round(bytes_step / secs / 1e9, 3), "unit": "GB/s", "cores": threads,
             "kind": "reference",
-            "sample": f"{tables} tables x 1 eviction cycle (16 decode_step incl. 1 trigger), "
-                      f"{secs:.2f} s wall"}
+            "sample": f"{tables} of the {args.config} tables x {cycles} eviction cycles (16 make_kv + "
+                      f"EvictionPolicy::decode_step each, one PagedEviction trigger), {secs:.3f} s timed "
+                      f"on {threads} threads; identity-prefilled to C (setup untimed)",
+            "evictions": int(ev)}
 
 
 # --------------------------------------------------------------------------- B200 arm
@@ -381,7 +411,8 @@ def run_b200(args, cfg, world, rank, local):
             "p50_evict_step_us": round(statistics.median(k2_ms) * 1e3, 2),
             "p50_evict_step_us_cached": round(k2c_us, 2),
             "roofline": {"bound": "hbm", "achieved": round(k2_gbs, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(k2_gbs / peak, 4), "traffic": None,
+                         "frac": round(k2_gbs / peak, 4), "traffic": ncu_traffic(),
+                         "traffic_source": "ncu dram__bytes_read+write per launch, profiles/*bench_launches*.csv",
                          "kernel": "K2 evict (plan + evict_score_kernel), per-layer launch",
                          "algorithmic_bytes_per_launch": k2_per_launch, "peak_kind": peak_kind},
             "prefill": prefill,

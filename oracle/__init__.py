@@ -321,7 +321,7 @@ class Reference:
         lib.ref_attend_table.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_uint32,
                                          C.c_uint32, C.c_void_p]
         lib.ref_bench_decode_cycles.argtypes = [C.c_size_t, C.c_size_t, C.c_uint32, C.c_uint32,
-                                                C.c_size_t, C.c_size_t, C.c_uint64, _dp,
+                                                C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint64, _dp,
                                                 C.POINTER(C.c_uint64)]
         lib.ref_bench_prefill.argtypes = [C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint32,
                                           C.c_uint32, C.c_size_t, C.c_uint64, _dp]
@@ -384,11 +384,16 @@ class Reference:
     def session(self, capacity, page_size, budget, n_tables, width, kind=PAGED_EVICTION):
         return RefSession(self, capacity, page_size, budget, n_tables, width, kind)
 
-    def bench_decode_cycles(self, n_tables, budget, page_size, w, threads, cycles, seed=1):
+    def bench_decode_cycles(self, n_tables, budget, page_size, w, threads, cycles, seed=1,
+                            warmup_cycles=0):
+        """Times `cycles` eviction cycles (after `warmup_cycles` untimed ones)
+        of the reference's decode_step on `n_tables` tables; returns
+        (seconds, page evictions in the timed cycles)."""
         secs = C.c_double()
         ev = C.c_uint64()
         self._check(self.lib.ref_bench_decode_cycles(n_tables, budget, page_size, w, threads,
-                                                     cycles, seed, C.byref(secs), C.byref(ev)))
+                                                     warmup_cycles, cycles, seed, C.byref(secs),
+                                                     C.byref(ev)))
         return secs.value, ev.value
 
     def bench_prefill(self, n_tables, L, budget, page_size, w, threads, seed=1):

@@ -453,8 +453,9 @@ extern "C" {
 // table triggers exactly one PagedEviction page eviction per cycle
 // (policy.cpp:143-155). Returns seconds; *evictions = Page decisions seen.
 int ref_bench_decode_cycles(std::size_t n_tables, std::size_t budget, std::uint32_t page_size,
-                            std::uint32_t w, std::size_t n_threads, std::size_t cycles,
-                            std::uint64_t seed, double* seconds, std::uint64_t* evictions) {
+                            std::uint32_t w, std::size_t n_threads, std::size_t warmup_cycles,
+                            std::size_t cycles, std::uint64_t seed, double* seconds,
+                            std::uint64_t* evictions) {
     return guarded([&] {
         n_threads = std::max<std::size_t>(1, std::min(n_threads, n_tables));
         PolicyConfig cfg;
@@ -462,9 +463,10 @@ int ref_bench_decode_cycles(std::size_t n_tables, std::size_t budget, std::uint3
         cfg.page_size = page_size;
         cfg.kind = PolicyKind::PagedEviction;
         std::vector<Worker> workers(n_threads);
-        // Pre-drawn decode inputs: one stream of cycles*B tokens per thread,
-        // re-used across that thread's tables.
-        const std::size_t steps = cycles * page_size;
+        // Pre-drawn decode inputs: one stream of (warmup+timed)*B tokens per
+        // thread, re-used across that thread's tables.
+        const std::size_t warm_steps = warmup_cycles * page_size;
+        const std::size_t steps = (warmup_cycles + cycles) * page_size;
         std::vector<std::vector<float>> dk(n_threads), dv(n_threads);
         std::vector<std::atomic<std::uint64_t>> ev(n_threads);
         std::vector<std::thread> setup;
@@ -494,10 +496,10 @@ int ref_bench_decode_cycles(std::size_t n_tables, std::size_t budget, std::uint3
             });
         }
         for (auto& x : setup) x.join();
-        *seconds = timed_parallel(n_threads, [&](std::size_t ti) {
+        auto run_steps = [&](std::size_t ti, std::size_t s0, std::size_t s1) {
             Worker& wk = workers[ti];
             std::uint64_t e = 0;
-            for (std::size_t st = 0; st < steps; ++st) {
+            for (std::size_t st = s0; st < s1; ++st) {
                 const float* kr = dk[ti].data() + st * w;
                 const float* vr = dv[ti].data() + st * w;
                 for (std::size_t j = 0; j < wk.tables.size(); ++j) {
@@ -508,8 +510,15 @@ int ref_bench_decode_cycles(std::size_t n_tables, std::size_t budget, std::uint3
                     e += d.kind == EvictionDecision::Kind::Page;
                 }
             }
-            ev[ti] = e;
-        });
+            return e;
+        };
+        if (warm_steps > 0) {  // untimed warm-up cycles
+            std::vector<std::thread> warm;
+            for (std::size_t ti = 0; ti < n_threads; ++ti)
+                warm.emplace_back([&, ti] { run_steps(ti, 0, warm_steps); });
+            for (auto& x : warm) x.join();
+        }
+        *seconds = timed_parallel(n_threads, [&](std::size_t ti) { ev[ti] = run_steps(ti, warm_steps, steps); });
         std::uint64_t tot = 0;
         for (auto& x : ev) tot += x.load();
         *evictions = tot;

@@ -220,16 +220,19 @@ __device__ __forceinline__ bool evict_triggered(const DevState& s, int t) {
            s.retained[t] > s.C;
 }
 
-// Grid-level completion: every CTA takes a ticket when it is done; the last
-// one pushes the launch's released pages on the free stack in ascending
-// table id (release, page_pool.cpp:35-38; canonical order DESIGN.md §1.6).
+// Launch-level completion: every TABLE of the launch takes one ticket when it
+// is settled (a non-triggered table at once, a triggered one after its
+// finalize); whoever takes the launch's last ticket pushes the launch's
+// released pages on the free stack in ascending table id (release,
+// page_pool.cpp:35-38; canonical order DESIGN.md §1.6). `settled` is
+// block-uniform.
 __device__ __forceinline__ void push_victims_if_last(const DevState& s, int n, int32_t* vpage,
-                                                     unsigned long long grid_last) {
+                                                     unsigned long long grid_last, int settled) {
     __shared__ int is_last;
     __shared__ int scan_sm[33];
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) is_last = (atomicAdd(s.grid_ctr, 1ull) == grid_last);
+    if (threadIdx.x == 0) is_last = settled > 0 && (atomicAdd(s.grid_ctr, (unsigned long long)settled) + settled - 1 >= grid_last);
     __syncthreads();
     if (!is_last) return;
     __threadfence();
@@ -269,10 +272,14 @@ __global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
     const bool trig = evict_triggered(s, t);
     const int N = s.num_pages[t];
     const int n_cta = (N + pages_per_cta - 1) / pages_per_cta;
+    int settled = 0;  // tables this CTA settles (block-uniform)
     if (!trig) {
-        if (c == 0 && threadIdx.x == 0) {
-            vpage[y] = -1;
-            if (victims) victims[y] = -1;
+        if (c == 0) {
+            settled = 1;
+            if (threadIdx.x == 0) {
+                vpage[y] = -1;
+                if (victims) victims[y] = -1;
+            }
         }
     } else if (c < n_cta) {
         const int p0 = c * pages_per_cta;
@@ -324,9 +331,10 @@ __global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
                 finalize_evict(s, t, y, N, scratch + (int64_t)y * s.max_pages, vpage, victims);
                 if (lane == 0) tickets[y] = 0;
             }
+            settled = 1;
         }
     }
-    push_victims_if_last(s, ts.size(s), vpage, grid_last);
+    push_victims_if_last(s, ts.size(s), vpage, grid_last, settled);
 }
 
 template <int SV>
@@ -383,7 +391,7 @@ __global__ void __launch_bounds__(256) evict_cached_kernel(DevState s, TableSet 
             finalize_evict(s, t, y, N, sc, vpage, victims);
         }
     }
-    push_victims_if_last(s, n, vpage, grid_last);
+    push_victims_if_last(s, n, vpage, grid_last, min(8, n - static_cast<int>(blockIdx.x) * 8));
 }
 
 }  // namespace pe

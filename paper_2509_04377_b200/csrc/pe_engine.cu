@@ -541,14 +541,14 @@ pe_status pe_decode_evict(pe_engine* e, int32_t layer_begin, int32_t n_layers, i
     // one launch: the grid's last CTA pushes the released pages in ascending
     // table id (no separate planner)
     if (mode == PE_SCORE_RECOMPUTE) {
+        // balanced chunks of <= kEvictPagesPerCta pages (257 pages -> 9 x 29)
         const int chunks = (s.max_pages + kEvictPagesPerCta - 1) / kEvictPagesPerCta;
-        const unsigned long long grid = (unsigned long long)n * chunks;
-        e->grid_tickets += grid;
-        launch_evict_score_any(e->variant, dim3(n, chunks), kEvictThreads, st, s, ts, kEvictPagesPerCta,
+        const int ppc = (s.max_pages + chunks - 1) / chunks;
+        e->grid_tickets += (unsigned long long)n;  // one completion ticket per table
+        launch_evict_score_any(e->variant, dim3(n, chunks), kEvictThreads, st, s, ts, ppc,
                                e->evict_scratch, e->tickets, e->vpage, vdst, e->grid_tickets - 1);
     } else {
-        const unsigned long long grid = (unsigned long long)(n + 7) / 8;
-        e->grid_tickets += grid;
+        e->grid_tickets += (unsigned long long)n;
         evict_cached_kernel<<<(n + 7) / 8, 256, 0, st>>>(s, ts, e->evict_scratch, e->vpage, vdst,
                                                           e->grid_tickets - 1);
     }
