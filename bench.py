@@ -14,8 +14,11 @@ Setup (untimed, but measured with CUDA events and reported under
 
 One bench STEP = one eviction cycle of the whole batch: B=16 decode tokens
 appended to every table (K0, one launch per token over all layers) followed
-by the PagedEviction block eviction of every table (K2, one launch per
-layer, pages rescored from their resident K/V bytes). `value` = algorithmic
+by the PagedEviction block eviction of every table (K2, pages rescored from
+their resident K/V bytes; by default ONE launch per decode step covering
+all layers — each table's decision depends only on that table, so a layer
+loop that evicts after the step is equivalent; `--evict-launch layer` runs
+one launch per layer, and the other granularity is reported too). `value` = algorithmic
 bytes of the step (K2: (C+B)*row + 8*(C/B+1) + 4 per table; K0: 2*row+4
 per table per token) / device time of the step, all ranks.
 
@@ -112,7 +115,7 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def ncu_traffic(kernel_substr="evict_score_kernel"):
+def ncu_traffic(kernel_substr="evict_score_kernel", expect_bytes=None):
     """Mean DRAM bytes (read+write) per launch of `kernel_substr` from the
     committed ncu launch list of this command (profiles/*bench_launches*.csv,
     `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
@@ -136,7 +139,10 @@ def ncu_traffic(kernel_substr="evict_score_kernel"):
             per[r[ii]] = per.get(r[ii], 0.0) + float(r[vi].replace(",", "")) * (
                 1e9 if "Gbyte" in r[hdr.index("Metric Unit")] else 1e6 if "Mbyte" in r[hdr.index("Metric Unit")]
                 else 1.0)
-    return round(sum(per.values()) / len(per)) if per else None
+    vals = list(per.values())
+    if expect_bytes:  # launches of the same size as the measured one (the list holds both granularities)
+        vals = [v for v in vals if 0.5 * expect_bytes < v < 2.0 * expect_bytes]
+    return round(sum(vals) / len(vals)) if vals else None
 
 
 # --------------------------------------------------------------------------- helpers
@@ -287,7 +293,7 @@ def run_b200(args, cfg, world, rank, local):
     k2_alg = n_tab * k2_bytes_per_table(C, row)          # per step (all layers)
     k0_alg = n_tab * B * (2 * row + 4)                   # read + write rows, positions
     step_bytes = k2_alg + k0_alg
-    k2_per_launch = n_tab_layer * k2_bytes_per_table(C, row)
+    k2_per_launch = (n_tab if args.evict_launch == "step" else n_tab_layer) * k2_bytes_per_table(C, row)
 
     def cycle(record=None, host=False, mode=pe.ScoreMode.RECOMPUTE, victims_host=None):
         for j in range(B):
@@ -296,15 +302,17 @@ def run_b200(args, cfg, world, rank, local):
             else:
                 eng.append_token(0, NL, rows_k[j], rows_v[j], pos)
             pos.add_(1)
-        for layer in range(NL):
+        spans = [(0, NL)] if args.evict_launch == "step" else [(layer, 1) for layer in range(NL)]
+        for l0, nl in spans:
+            vh = victims_host[: nl * n_tab_layer] if victims_host is not None else None
             if record is not None:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                eng.evict(layer, 1, step=0, mode=mode, victims=victims_host)
+                eng.evict(l0, nl, step=0, mode=mode, victims=vh)
                 b.record(stream)
                 record.append((a, b))
             else:
-                eng.evict(layer, 1, step=0, mode=mode, victims=victims_host)
+                eng.evict(l0, nl, step=0, mode=mode, victims=vh)
 
     def barrier():
         if world > 1:
@@ -346,8 +354,20 @@ def run_b200(args, cfg, world, rank, local):
     eng.sync()
     k2c_us = statistics.median([a.elapsed_time(b) * 1e3 for a, b in evc])
 
+    # ---------------- the other launch granularity, for reference
+    other = "layer" if args.evict_launch == "step" else "step"
+    saved = args.evict_launch
+    args.evict_launch = other
+    evo = []
+    for _ in range(2):
+        cycle(record=evo)
+    eng.sync()
+    args.evict_launch = saved
+    other_us = statistics.median([a.elapsed_time(b) * 1e3 for a, b in evo])
+    other_bytes = (n_tab if other == "step" else n_tab_layer) * k2_bytes_per_table(C, row)
+
     # ---------------- e2e: host buffers through the C-ABI
-    vict_host = torch.zeros(n_tab_layer, dtype=torch.int32).pin_memory()  # step result read back
+    vict_host = torch.zeros(n_tab, dtype=torch.int32).pin_memory()  # step result read back
     cycle(host=True, victims_host=vict_host)  # warm the host-staging ring (untimed)
     eng.sync()
     barrier()
@@ -359,7 +379,7 @@ def run_b200(args, cfg, world, rank, local):
     e2e_s = max_over_ranks((time.perf_counter() - w0) / max(1, args.steps // 2))
     e2e = {"value": round(world * step_bytes / e2e_s / 1e9, 3), "unit": "GB/s",
            "h2d_bytes_per_step": int(B * 2 * NL * S * H * d * elt + B * S * 8),
-           "d2h_bytes_per_step": int(NL * n_tab_layer * 4),
+           "d2h_bytes_per_step": int(n_tab * 4),
            "ms_per_step": round(e2e_s * 1e3, 3)}
 
     # ---------------- pruned decode tokens/s (K0 + K2 + K3, all layers)
@@ -404,16 +424,21 @@ def run_b200(args, cfg, world, rank, local):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic N(0,1) K/V/Q (torch.randn); inputs resident in HBM",
             "config": {"workload": f"{args.config}: {cfg['desc']}", "tables_per_gpu": n_tab,
-                       "page_size": B, "step": "one eviction cycle: 16 decode appends (K0) + "
-                       "block eviction of every table (K2, per-layer launches)",
+                       "page_size": B, "step": "one eviction cycle: 16 decode appends (K0, all layers per launch) "
+                       "+ block eviction of every table (K2, " + ("one launch for all layers)" if args.evict_launch
+                                                                  == "step" else "one launch per layer)"),
                        "l2": "inputs larger than L2 (pool %.1f GB per GPU)" % (eng.info().pool_bytes / 1e9)},
             "pct_of_peak": round(100 * value / world / peak, 2),
             "p50_evict_step_us": round(statistics.median(k2_ms) * 1e3, 2),
             "p50_evict_step_us_cached": round(k2c_us, 2),
+            "evict_launch": args.evict_launch,
+            f"p50_evict_{other}_launch_us": round(other_us, 2),
+            f"evict_{other}_launch_gbs": round(other_bytes / (other_us * 1e-6) / 1e9, 1),
             "roofline": {"bound": "hbm", "achieved": round(k2_gbs, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(k2_gbs / peak, 4), "traffic": ncu_traffic(),
+                         "frac": round(k2_gbs / peak, 4), "traffic": ncu_traffic(expect_bytes=k2_per_launch),
                          "traffic_source": "ncu dram__bytes_read+write per launch, profiles/*bench_launches*.csv",
-                         "kernel": "K2 evict (plan + evict_score_kernel), per-layer launch",
+                         "kernel": "K2 evict_score_kernel, " + ("one launch per decode step (all 32 layers)"
+                                                                  if args.evict_launch == "step" else "per-layer launch"),
                          "algorithmic_bytes_per_launch": k2_per_launch, "peak_kind": peak_kind},
             "prefill": prefill,
             "decode": decode,
@@ -439,6 +464,8 @@ def main():
     ap.add_argument("--ref-tables", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--evict-launch", default="step", choices=["layer", "step"],
+                    help="one K2 launch per layer, or one per decode step covering all layers")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
