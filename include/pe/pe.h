@@ -205,6 +205,59 @@ typedef struct pe_device_view {
 } pe_device_view;
 pe_status pe_get_device_view(pe_engine* eng, pe_device_view* out);
 
+/* ------------------------------------------------------------------------
+ * Table-granular API: the reference's per-object calls, one BlockTable per
+ * table id. This is what the C++ façade (include/pe/pagedevict.hpp,
+ * libpagedevict_b200.so) binds; appends and PagedEviction decisions go
+ * through the same kernels as the batched calls (K0, K2/K2c) with an
+ * explicit table list. Table lists are HOST arrays of strictly ascending ids
+ * (the canonical order); row i of k_rows/v_rows/positions belongs to
+ * table_ids[i]. Device-side failures set the status word read by pe_sync.
+ * ---------------------------------------------------------------------- */
+
+/* BlockTable::append_token for each listed table (block_table.cpp:10-19):
+ * writes into the newest page's next slot, opening a page (PagePool::allocate,
+ * page_pool.cpp:24-33) when the newest page is write-full or none exists.
+ * Pool exhaustion -> PE_POOL_EXHAUSTED at pe_sync; tables before the failing
+ * one (ascending id) are appended, later ones are not (reference loop order). */
+pe_status pe_table_append(pe_engine* eng, int32_t n, const int32_t* table_ids, const void* k_rows,
+                          const void* v_rows, const int64_t* positions, void* stream);
+
+/* PagedEvictionPolicy::evict (policy.cpp:143-155) with C = cache_budget for
+ * each listed table: trigger iff the newest page is write-full and
+ * retained > C; then score_pages -> rank_pages -> free_page. victims
+ * (nullable, host or device) [n] receives the evicted logical index or -1. */
+pe_status pe_table_evict(pe_engine* eng, int32_t n, const int32_t* table_ids, int32_t cache_budget,
+                         int32_t mode, int32_t* victims, void* stream);
+
+/* BlockTable::free_page (block_table.cpp:21-31): releases the page at
+ * logical_index whole, later entries close ranks. Out of range ->
+ * PE_INDEX_OUT_OF_RANGE at pe_sync (no-op). */
+pe_status pe_table_free_page(pe_engine* eng, int32_t table, int32_t logical_index, void* stream);
+
+/* BlockTable::clear (block_table.cpp:72-78): releases every mapped page in
+ * logical order. */
+pe_status pe_table_clear(pe_engine* eng, int32_t table, void* stream);
+
+/* attend_detailed (attention.cpp:15-99) over one table: per head h, softmax
+ * of q_h.k_h/sqrt(head_dim) over the retained tokens in logical order,
+ * heads concatenated in the row (head h = elements [h*head_dim, (h+1)*head_dim)).
+ * Double-precision in the reference's order (bit-identical up to the last
+ * ulp of exp). query float32 [head_count*head_dim]; out float32 (same
+ * length); weight_sums (nullable) double [head_count]. No retained token ->
+ * PE_EMPTY_CACHE; head_count*head_dim wider than the rows -> PE_LENGTH_MISMATCH. */
+pe_status pe_table_attend(pe_engine* eng, int32_t table, const float* query, int32_t head_count,
+                          int32_t head_dim, float* out, double* weight_sums, void* stream);
+
+/* One table's block-table row (page_ids [num_pages], nullable) and counters. */
+pe_status pe_read_table(pe_engine* eng, int32_t table, int32_t* page_ids, int32_t* num_pages,
+                        int32_t* newest_fill, int32_t* retained);
+
+/* PagePool::allocate / release (page_pool.cpp:24-38) on the device free
+ * list, synchronous. Empty list -> PE_POOL_EXHAUSTED. */
+pe_status pe_pool_allocate(pe_engine* eng, int32_t* page_id);
+pe_status pe_pool_release(pe_engine* eng, int32_t page_id);
+
 /* Thread-local message for the last non-OK status returned on this thread. */
 const char* pe_last_error(void);
 const char* pe_status_string(pe_status s);

@@ -19,7 +19,11 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libpe_b200.so"
-SOURCES = ["pe_engine.cu", "pe_decode.cu", "pe_prefill.cu", "pe_attention.cu"]
+# C++ façade: the reference's pagedevict:: API over the C-ABI
+FACADE_SRC = PKG / "cpp" / "pagedevict.cpp"
+FACADE_HDR = ROOT / "include" / "pe" / "pagedevict.hpp"
+FACADE_LIB = LIB_DIR / "libpagedevict_b200.so"
+SOURCES = ["pe_engine.cu", "pe_decode.cu", "pe_prefill.cu", "pe_attention.cu", "pe_table.cu"]
 HEADERS = ["pe_internal.cuh", "pe_kernels.cuh", "pe_score.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -43,8 +47,25 @@ def stale() -> bool:
     return any(p.stat().st_mtime > t for p in inputs())
 
 
+def build_facade(force: bool = False) -> Path:
+    """g++ -std=c++20 the façade into libpagedevict_b200.so (links libpe_b200.so, rpath $ORIGIN)."""
+    if (not force and FACADE_LIB.exists() and
+            FACADE_LIB.stat().st_mtime >= max(p.stat().st_mtime for p in (FACADE_SRC, FACADE_HDR, LIB))):
+        return FACADE_LIB
+    tmp = FACADE_LIB.with_suffix(".so.tmp")
+    cmd = ["g++", "-std=c++20", "-O2", "-g", "-fPIC", "-shared", "-Wall", "-Wextra",
+           f"-I{ROOT / 'include'}", str(FACADE_SRC), f"-L{LIB_DIR}", "-lpe_b200",
+           "-Wl,-rpath,$ORIGIN", "-o", str(tmp)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"g++ failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stderr[-6000:]}")
+    os.replace(tmp, FACADE_LIB)
+    return FACADE_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not stale():
+        build_facade()
         return LIB
     LIB_DIR.mkdir(parents=True, exist_ok=True)
     tmp = LIB.with_suffix(".so.tmp")
@@ -61,6 +82,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if verbose:
         print(res.stderr)
     os.replace(tmp, LIB)
+    build_facade(force=True)
     return LIB
 
 

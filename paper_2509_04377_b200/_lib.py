@@ -59,6 +59,15 @@ SIGNATURES = {
     "pe_read_positions": (C.c_int, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "pe_read_pages": (C.c_int, [c_vp, c_i32, c_i32, c_vp]),
     "pe_get_device_view": (C.c_int, [c_vp, C.POINTER(PeDeviceView)]),
+    # table-granular API (the C++ façade's calls)
+    "pe_table_append": (C.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pe_table_evict": (C.c_int, [c_vp, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "pe_table_free_page": (C.c_int, [c_vp, c_i32, c_i32, c_vp]),
+    "pe_table_clear": (C.c_int, [c_vp, c_i32, c_vp]),
+    "pe_table_attend": (C.c_int, [c_vp, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
+    "pe_read_table": (C.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "pe_pool_allocate": (C.c_int, [c_vp, C.POINTER(c_i32)]),
+    "pe_pool_release": (C.c_int, [c_vp, c_i32]),
 }
 
 

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
                                           served ? vdst : nullptr);
     if (served && q == 0) {
         const int64_t ps = (int64_t)page * s.B + slot;
-        s.positions[ps] = static_cast<int32_t>(positions[ts.input_row(s, my_i) / s.tab_heads % s.n_seqs]);
+        s.positions[ps] = static_cast<int32_t>(positions[ts.pos_index(s, my_i)]);
         s.token_scores[ps] = S;
         s.newest_fill[t] = slot + 1;
         s.retained[t] += 1;

@@ -101,6 +101,14 @@ struct pe_engine {
     size_t out_stage_elems = 0;
     pe_stats stats{};
     int max_dyn_prefill = 0, max_dyn_attn = 0;
+    // table-granular API (pe_table_*, pe_pool_*)
+    int32_t* alloc_out = nullptr;
+    double* attend_logits = nullptr;
+    size_t attend_logits_elems = 0;
+    float* attend_out = nullptr;
+    size_t attend_out_elems = 0;
+    double* attend_ws = nullptr;
+    size_t attend_ws_elems = 0;
 };
 
 namespace {
@@ -277,6 +285,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         dalloc(&s.top, 1) != cudaSuccess || dalloc(&s.status, 1) != cudaSuccess ||
         dalloc(&s.evict_count, 1) != cudaSuccess || dalloc(&s.grid_ctr, 1) != cudaSuccess ||
         dalloc(&e->vpage, n_tables) != cudaSuccess || dalloc(&e->ctl, 1) != cudaSuccess ||
+        dalloc(&e->alloc_out, 1) != cudaSuccess ||
         dalloc(&e->lb_status, (size_t)n_tables / 64 + 2) != cudaSuccess ||
         dalloc(&e->rank, n_tables) != cudaSuccess || dalloc(&e->work, n_tables) != cudaSuccess ||
         dalloc(&e->victims, n_tables) != cudaSuccess || dalloc(&e->tickets, n_tables) != cudaSuccess ||
@@ -365,7 +374,8 @@ pe_status pe_engine_destroy(pe_engine* e) {
                    e->ctl, e->rank,
                    e->work, e->victims, e->tickets, e->evict_scratch, e->tab_len, e->tab_tok0,
                    e->tab_pagebase, e->evicted_dev, e->part_o,
-                   e->part_ml, e->out_stage, e->tab_keybase, e->keys, e->surv, e->lb_status};
+                   e->part_ml, e->out_stage, e->tab_keybase, e->keys, e->surv, e->lb_status,
+                   e->alloc_out, e->attend_logits, e->attend_out, e->attend_ws};
     for (void* p : dev) {
         if (p) cudaFree(p);
     }
@@ -487,6 +497,65 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     return PE_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// One eviction launch over table set `ts` (state `sc`: the engine's, or a
+// copy with the table API's per-call budget).
+pe_status launch_evict(pe_engine* e, const DevState& sc, const TableSet& ts, int32_t mode, int32_t* victims,
+                       cudaStream_t st) {
+    const int n = ts.size(sc);
+    const bool vic_dev = victims && is_device_ptr(victims);
+    int32_t* vdst = vic_dev ? victims : e->victims;
+    // one launch: the grid's last CTA pushes the released pages in ascending
+    // table id (no separate planner)
+    if (mode == PE_SCORE_RECOMPUTE) {
+        // balanced chunks of <= kEvictPagesPerCta pages (257 pages -> 9 x 29)
+        const int chunks = (sc.max_pages + kEvictPagesPerCta - 1) / kEvictPagesPerCta;
+        const int ppc = (sc.max_pages + chunks - 1) / chunks;
+        e->grid_tickets += (unsigned long long)n;  // one completion ticket per table
+        launch_evict_score_any(e->variant, dim3(n, chunks), kEvictThreads, st, sc, ts, ppc,
+                               e->evict_scratch, e->tickets, e->vpage, vdst, e->grid_tickets - 1);
+    } else {
+        e->grid_tickets += (unsigned long long)n;
+        evict_cached_kernel<<<(n + 7) / 8, 256, 0, st>>>(sc, ts, e->evict_scratch, e->vpage, vdst,
+                                                           e->grid_tickets - 1);
+    }
+    pe_status r = check_launch(e, "evict kernel");
+    if (r != PE_OK) return r;
+    e->stats.kernel_launches += 1;
+    e->stats.evict_calls += 1;
+    if (victims && !vic_dev) {
+        PE_CUDA(cudaMemcpyAsync(victims, e->victims, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    }
+    return PE_OK;
+}
+
+// One append launch (K0) over table set `ts`; k/v/positions already on the device.
+pe_status launch_append(pe_engine* e, const TableSet& ts, const uint8_t* dk, const uint8_t* dv,
+                        const int64_t* dp, cudaStream_t st) {
+    const DevState& s = e->s;
+    const int n = ts.size(s);
+    // one launch: canonical pop ranks by a single-pass decoupled look-back
+    const int warps = kAppendThreads / 32;
+    const int blocks = (n + 16 * warps - 1) / (16 * warps);
+    const unsigned long long ticket_base = e->grid_tickets;
+    e->grid_tickets += blocks;
+    e->append_epoch = (e->append_epoch % 0x3FFFFFFF) + 1;
+    launch_append_any(e->variant, blocks, st, s, ts, dk, dv, dp, e->lb_status, e->ctl, ticket_base, e->append_epoch);
+    mark_consumed(e, st);
+    pe_status r = check_launch(e, "append_kernel");
+    if (r != PE_OK) return r;
+    e->stats.kernel_launches += 1;
+    e->stats.append_calls += 1;
+    return PE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 // ------------------------------------------------------------------ K0
 pe_status pe_decode_append(pe_engine* e, int32_t layer_begin, int32_t n_layers, const void* k_rows,
                            const void* v_rows, const int64_t* positions, void* stream) {
@@ -507,20 +576,7 @@ pe_status pe_decode_append(pe_engine* e, int32_t layer_begin, int32_t n_layers, 
     if (r != PE_OK) return r;
     r = as_device(e, positions, sizeof(int64_t) * s.n_seqs, st, &dp);
     if (r != PE_OK) return r;
-    // one launch: canonical pop ranks by a single-pass decoupled look-back
-    const int warps = kAppendThreads / 32;
-    const int blocks = (n + 16 * warps - 1) / (16 * warps);
-    const unsigned long long ticket_base = e->grid_tickets;
-    e->grid_tickets += blocks;
-    e->append_epoch = (e->append_epoch % 0x3FFFFFFF) + 1;
-    launch_append_any(e->variant, blocks, st, s, ts, dk, dv, reinterpret_cast<const int64_t*>(dp), e->lb_status,
-                      e->ctl, ticket_base, e->append_epoch);
-    mark_consumed(e, st);
-    r = check_launch(e, "append_kernel");
-    if (r != PE_OK) return r;
-    e->stats.kernel_launches += 1;
-    e->stats.append_calls += 1;
-    return PE_OK;
+    return launch_append(e, ts, dk, dv, reinterpret_cast<const int64_t*>(dp), st);
 }
 
 // ------------------------------------------------------------------ K2 / K2c
@@ -533,33 +589,8 @@ pe_status pe_decode_evict(pe_engine* e, int32_t layer_begin, int32_t n_layers, i
         return fail(PE_INVALID_ARG, "layer range out of range");
     if (mode != PE_SCORE_RECOMPUTE && mode != PE_SCORE_CACHED) return fail(PE_INVALID_ARG, "score mode");
     cudaSetDevice(e->device);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     TableSet ts{layer_begin, n_layers};
-    const int n = ts.size(s);
-    const bool vic_dev = victims && is_device_ptr(victims);
-    int32_t* vdst = vic_dev ? victims : e->victims;
-    // one launch: the grid's last CTA pushes the released pages in ascending
-    // table id (no separate planner)
-    if (mode == PE_SCORE_RECOMPUTE) {
-        // balanced chunks of <= kEvictPagesPerCta pages (257 pages -> 9 x 29)
-        const int chunks = (s.max_pages + kEvictPagesPerCta - 1) / kEvictPagesPerCta;
-        const int ppc = (s.max_pages + chunks - 1) / chunks;
-        e->grid_tickets += (unsigned long long)n;  // one completion ticket per table
-        launch_evict_score_any(e->variant, dim3(n, chunks), kEvictThreads, st, s, ts, ppc,
-                               e->evict_scratch, e->tickets, e->vpage, vdst, e->grid_tickets - 1);
-    } else {
-        e->grid_tickets += (unsigned long long)n;
-        evict_cached_kernel<<<(n + 7) / 8, 256, 0, st>>>(s, ts, e->evict_scratch, e->vpage, vdst,
-                                                          e->grid_tickets - 1);
-    }
-    pe_status r = check_launch(e, "evict kernel");
-    if (r != PE_OK) return r;
-    e->stats.kernel_launches += 1;
-    e->stats.evict_calls += 1;
-    if (victims && !vic_dev) {
-        PE_CUDA(cudaMemcpyAsync(victims, e->victims, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
-    }
-    return PE_OK;
+    return launch_evict(e, s, ts, mode, victims, static_cast<cudaStream_t>(stream));
 }
 
 pe_status pe_decode_step(pe_engine* e, int32_t layer_begin, int32_t n_layers, const void* k_rows,
@@ -757,6 +788,166 @@ pe_status pe_get_device_view(pe_engine* e, pe_device_view* out) {
     out->retained = e->s.retained;
     out->positions = e->s.positions;
     return PE_OK;
+}
+
+// ------------------------------------------------------------------ table-granular API
+}  // extern "C"
+
+namespace {
+
+pe_status check_table_list(pe_engine* e, int32_t n, const int32_t* ids) {
+    if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
+    if (n <= 0 || n > e->s.n_tables) return fail(PE_INVALID_ARG, "table count out of range");
+    if (ids == nullptr) return fail(PE_INVALID_ARG, "null table list");
+    if (is_device_ptr(ids)) return fail(PE_INVALID_ARG, "table list must be a host array");
+    for (int32_t i = 0; i < n; ++i) {
+        if (ids[i] < 0 || ids[i] >= e->s.n_tables) return fail(PE_INDEX_OUT_OF_RANGE, "table id out of range");
+        if (i > 0 && ids[i] <= ids[i - 1]) return fail(PE_INVALID_ARG, "table ids must be strictly ascending");
+    }
+    return PE_OK;
+}
+
+pe_status check_table(pe_engine* e, int32_t t) {
+    if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
+    if (t < 0 || t >= e->s.n_tables) return fail(PE_INDEX_OUT_OF_RANGE, "table id out of range");
+    return PE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+pe_status pe_table_append(pe_engine* e, int32_t n, const int32_t* table_ids, const void* k_rows,
+                          const void* v_rows, const int64_t* positions, void* stream) {
+    pe_status r = check_table_list(e, n, table_ids);
+    if (r != PE_OK) return r;
+    const DevState& s = e->s;
+    cudaSetDevice(e->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t bytes = (size_t)n * s.row_bytes;
+    const uint8_t *dk = nullptr, *dv = nullptr, *dp = nullptr, *di = nullptr;
+    e->n_pending = 0;
+    if ((r = as_device(e, table_ids, sizeof(int32_t) * n, st, &di)) != PE_OK) return r;
+    if ((r = as_device(e, k_rows, bytes, st, &dk)) != PE_OK) return r;
+    if ((r = as_device(e, v_rows, bytes, st, &dv)) != PE_OK) return r;
+    if ((r = as_device(e, positions, sizeof(int64_t) * n, st, &dp)) != PE_OK) return r;
+    TableSet ts{0, 1, reinterpret_cast<const int32_t*>(di), n};
+    return launch_append(e, ts, dk, dv, reinterpret_cast<const int64_t*>(dp), st);
+}
+
+pe_status pe_table_evict(pe_engine* e, int32_t n, const int32_t* table_ids, int32_t cache_budget, int32_t mode,
+                         int32_t* victims, void* stream) {
+    pe_status r = check_table_list(e, n, table_ids);
+    if (r != PE_OK) return r;
+    if (cache_budget < 0) return fail(PE_BUDGET_INVALID, "negative budget");
+    if (mode != PE_SCORE_RECOMPUTE && mode != PE_SCORE_CACHED) return fail(PE_INVALID_ARG, "score mode");
+    cudaSetDevice(e->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint8_t* di = nullptr;
+    e->n_pending = 0;
+    if ((r = as_device(e, table_ids, sizeof(int32_t) * n, st, &di)) != PE_OK) return r;
+    DevState sc = e->s;  // PagedEviction decision with this call's budget C
+    sc.policy = PE_POLICY_PAGED_EVICTION;
+    sc.C = cache_budget;
+    TableSet ts{0, 1, reinterpret_cast<const int32_t*>(di), n};
+    r = launch_evict(e, sc, ts, mode, victims, st);
+    mark_consumed(e, st);
+    return r;
+}
+
+pe_status pe_table_free_page(pe_engine* e, int32_t table, int32_t logical_index, void* stream) {
+    pe_status r = check_table(e, table);
+    if (r != PE_OK) return r;
+    cudaSetDevice(e->device);
+    table_free_page_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(e->s, table, logical_index);
+    e->stats.kernel_launches += 1;
+    return check_launch(e, "table_free_page_kernel");
+}
+
+pe_status pe_table_clear(pe_engine* e, int32_t table, void* stream) {
+    pe_status r = check_table(e, table);
+    if (r != PE_OK) return r;
+    cudaSetDevice(e->device);
+    table_clear_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(e->s, table);
+    e->stats.kernel_launches += 1;
+    return check_launch(e, "table_clear_kernel");
+}
+
+pe_status pe_table_attend(pe_engine* e, int32_t table, const float* query, int32_t head_count, int32_t head_dim,
+                          float* out, double* weight_sums, void* stream) {
+    pe_status r = check_table(e, table);
+    if (r != PE_OK) return r;
+    const DevState& s = e->s;
+    if (query == nullptr || out == nullptr) return fail(PE_INVALID_ARG, "null buffer");
+    if (head_count <= 0 || head_dim <= 0 || (int64_t)head_count * head_dim > s.w)
+        return fail(PE_LENGTH_MISMATCH, "head_count * head_dim exceeds the pool row width");
+    cudaSetDevice(e->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int32_t R = 0;
+    PE_CUDA(cudaStreamSynchronize(st));
+    PE_CUDA(cudaMemcpy(&R, s.retained + table, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (R <= 0) return fail(PE_EMPTY_CACHE, "attention requires at least one retained token");
+    const size_t width = (size_t)head_count * head_dim;
+    e->n_pending = 0;
+    const uint8_t* dq = nullptr;
+    if ((r = as_device(e, query, sizeof(float) * width, st, &dq)) != PE_OK) return r;
+    if ((r = ensure_t(&e->attend_logits, &e->attend_logits_elems, (size_t)R * head_count)) != PE_OK) return r;
+    if ((r = ensure_t(&e->attend_out, &e->attend_out_elems, width)) != PE_OK) return r;
+    if ((r = ensure_t(&e->attend_ws, &e->attend_ws_elems, (size_t)head_count)) != PE_OK) return r;
+    const bool out_dev = is_device_ptr(out);
+    const bool ws_dev = weight_sums && is_device_ptr(weight_sums);
+    table_attend_kernel<<<head_count, 256, 0, st>>>(s, table, reinterpret_cast<const float*>(dq), head_dim,
+                                                    e->attend_logits, out_dev ? out : e->attend_out,
+                                                    weight_sums ? (ws_dev ? weight_sums : e->attend_ws) : nullptr);
+    mark_consumed(e, st);
+    if ((r = check_launch(e, "table_attend_kernel")) != PE_OK) return r;
+    e->stats.kernel_launches += 1;
+    e->stats.attention_calls += 1;
+    if (!out_dev) PE_CUDA(cudaMemcpyAsync(out, e->attend_out, sizeof(float) * width, cudaMemcpyDeviceToHost, st));
+    if (weight_sums && !ws_dev)
+        PE_CUDA(cudaMemcpyAsync(weight_sums, e->attend_ws, sizeof(double) * head_count, cudaMemcpyDeviceToHost, st));
+    return PE_OK;
+}
+
+pe_status pe_read_table(pe_engine* e, int32_t table, int32_t* page_ids, int32_t* num_pages, int32_t* newest_fill,
+                        int32_t* retained) {
+    pe_status r = check_table(e, table);
+    if (r != PE_OK) return r;
+    const DevState& s = e->s;
+    cudaSetDevice(e->device);
+    PE_CUDA(cudaDeviceSynchronize());
+    int32_t np = 0;
+    PE_CUDA(cudaMemcpy(&np, s.num_pages + table, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (num_pages) *num_pages = np;
+    if (page_ids && np > 0)
+        PE_CUDA(cudaMemcpy(page_ids, s.block_table + (size_t)table * s.max_pages, sizeof(int32_t) * np,
+                           cudaMemcpyDeviceToHost));
+    if (newest_fill) PE_CUDA(cudaMemcpy(newest_fill, s.newest_fill + table, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (retained) PE_CUDA(cudaMemcpy(retained, s.retained + table, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    return PE_OK;
+}
+
+pe_status pe_pool_allocate(pe_engine* e, int32_t* page_id) {
+    if (e == nullptr || page_id == nullptr) return fail(PE_INVALID_ARG, "null argument");
+    cudaSetDevice(e->device);
+    pool_allocate_kernel<<<1, 1>>>(e->s, e->alloc_out);
+    pe_status r = check_launch(e, "pool_allocate_kernel");
+    if (r != PE_OK) return r;
+    e->stats.kernel_launches += 1;
+    if ((r = pe_sync(e)) != PE_OK) return r;
+    PE_CUDA(cudaMemcpy(page_id, e->alloc_out, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    return PE_OK;
+}
+
+pe_status pe_pool_release(pe_engine* e, int32_t page_id) {
+    if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
+    if (page_id < 0 || page_id >= e->s.capacity) return fail(PE_INDEX_OUT_OF_RANGE, "page id out of range");
+    cudaSetDevice(e->device);
+    pool_release_kernel<<<1, 1>>>(e->s, page_id);
+    pe_status r = check_launch(e, "pool_release_kernel");
+    if (r != PE_OK) return r;
+    e->stats.kernel_launches += 1;
+    return pe_sync(e);
 }
 
 }  // extern "C"

@@ -49,11 +49,22 @@ struct LaunchCtl {
 
 // Launch table set: decode launches cover every sequence for layers
 // [layer_begin, layer_begin+n_layers); index i enumerates (seq, layer, head)
-// seq-major, which is ascending table id.
+// seq-major, which is ascending table id. The table-granular API (pe_table_*,
+// one reference BlockTable per call entry) instead passes an explicit
+// ascending id list `ids` (device) whose entry i reads input row i.
 struct TableSet {
     int32_t layer_begin, n_layers;
-    __host__ __device__ int32_t size(const DevState& s) const { return s.n_seqs * n_layers * s.tab_heads; }
+    const int32_t* ids = nullptr;
+    int32_t n_ids = 0;
+    __host__ __device__ int32_t size(const DevState& s) const {
+        return ids ? n_ids : s.n_seqs * n_layers * s.tab_heads;
+    }
+    // index into the launch's positions array
+    __host__ __device__ int64_t pos_index(const DevState& s, int32_t i) const {
+        return ids ? i : input_row(s, i) / s.tab_heads % s.n_seqs;
+    }
     __host__ __device__ int32_t table(const DevState& s, int32_t i) const {
+        if (ids) return ids[i];
         const int32_t h = i % s.tab_heads;
         const int32_t rest = i / s.tab_heads;
         const int32_t li = rest % n_layers;
@@ -62,6 +73,7 @@ struct TableSet {
     }
     // row index of launch table i in an input laid out [n_layers][n_seqs][tab_heads]
     __host__ __device__ int64_t input_row(const DevState& s, int32_t i) const {
+        if (ids) return i;
         const int32_t h = i % s.tab_heads;
         const int32_t rest = i / s.tab_heads;
         const int32_t li = rest % n_layers;

@@ -64,4 +64,12 @@ void launch_attention_mma(int d, dim3 grid, size_t smem, cudaStream_t st, const 
 const void* attention_mma_fn(int d);
 __global__ void attention_merge_kernel(DevState s, AttnArgs a);
 
+// table-granular kernels (pe_table.cu)
+__global__ void pool_allocate_kernel(DevState s, int32_t* out);
+__global__ void pool_release_kernel(DevState s, int32_t id);
+__global__ void table_free_page_kernel(DevState s, int32_t t, int32_t idx);
+__global__ void table_clear_kernel(DevState s, int32_t t);
+__global__ void table_attend_kernel(DevState s, int32_t t, const float* q, int32_t head_dim, double* logits,
+                                    float* out, double* weight_sums);
+
 }  // namespace pe

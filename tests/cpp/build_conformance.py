@@ -1,0 +1,69 @@
+"""Builds the C++ façade conformance binaries (test infrastructure).
+
+ref_conformance: the reference's OWN unit tests for the cache-manager API
+(/root/reference/proj/tests/test_{paged_store,importance,policies,attention}.cpp),
+compiled unchanged against the B200 façade headers (include/pagedevict/*.hpp
+-> include/pe/pagedevict.hpp) with the doctest shim (tests/cpp/doctest.h)
+and linked to libpagedevict_b200.so. The reference's test-only helpers
+(tests/oracles.hpp, core/include/pagedevict/rng.hpp) are found through
+include paths placed AFTER ours, so every hot-path header resolves to the
+façade. The binary is built here (the reference tree is read at build time
+only), is git-ignored and travels to the GPU box with the repo snapshot.
+
+facade_tests: our own façade tests (tests/cpp/test_facade.cpp).
+"""
+from __future__ import annotations
+
+import subprocess
+import sys
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parent.parent
+OUT = HERE / "_build"
+LIB_DIR = ROOT / "paper_2509_04377_b200" / "lib"
+REF = Path("/root/reference/proj")
+REF_TESTS = ["test_paged_store.cpp", "test_importance.cpp", "test_policies.cpp", "test_attention.cpp"]
+
+
+def _cxx(srcs: list[Path], out: Path, extra_inc: list[Path]) -> Path:
+    OUT.mkdir(parents=True, exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-g", f"-I{HERE}", f"-I{ROOT / 'include'}",
+           *[f"-I{p}" for p in extra_inc], *map(str, srcs), str(HERE / "shim_main.cpp"),
+           f"-L{LIB_DIR}", "-lpagedevict_b200", "-lpe_b200", f"-Wl,-rpath,{LIB_DIR}",
+           "-Wl,-rpath,$ORIGIN/../../../paper_2509_04377_b200/lib", "-lpthread", "-o", str(out)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"g++ failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stderr[-8000:]}")
+    return out
+
+
+def build_reference_conformance() -> Path | None:
+    if not REF.exists():
+        return None
+    srcs = [REF / "tests" / t for t in REF_TESTS]
+    return _cxx(srcs, OUT / "ref_conformance", [REF / "tests", REF / "core" / "include"])
+
+
+def build_facade_tests() -> Path:
+    OUT.mkdir(parents=True, exist_ok=True)
+    obj = OUT / "pe_oracle.o"  # the C restatement, linked as the checker
+    cmd = ["gcc", "-std=c11", "-O2", "-fno-fast-math", "-ffp-contract=off", "-c", str(ROOT / "oracle" / "pe_oracle.c"), "-o", str(obj)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"gcc failed:\n{res.stderr[-4000:]}")
+    return _cxx([HERE / "test_facade.cpp", obj], OUT / "facade_tests", [])
+
+
+def build_all() -> None:
+    from paper_2509_04377_b200 import _build
+
+    _build.build()
+    build_facade_tests()
+    build_reference_conformance()
+
+
+if __name__ == "__main__":
+    sys.path.insert(0, str(ROOT))
+    build_all()
+    print("built", sorted(p.name for p in OUT.iterdir()))

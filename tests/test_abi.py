@@ -78,3 +78,26 @@ def test_policy_mirror():
     with pytest.raises(pe.BudgetInvalid):
         pe.PolicyConfig(cache_budget=8).validate()
     pe.PolicyConfig(cache_budget=4096).validate()
+
+
+def test_facade_library_exports_the_reference_api():
+    """libpagedevict_b200.so (the C++ façade) exports the reference's
+    pagedevict:: entry points and links the C-ABI engine."""
+    import subprocess
+
+    from paper_2509_04377_b200 import _build
+
+    _build.build()
+    lib = _build.FACADE_LIB
+    assert lib.exists()
+    syms = subprocess.run(["nm", "-DC", "--defined-only", str(lib)], capture_output=True, text=True).stdout
+    for sym in ("pagedevict::PagePool::PagePool", "pagedevict::PagePool::allocate",
+                "pagedevict::BlockTable::append_token", "pagedevict::BlockTable::free_page",
+                "pagedevict::BlockTable::retained_positions", "pagedevict::EvictionPolicy::prefill_compress",
+                "pagedevict::EvictionPolicy::decode_step", "pagedevict::make_policy",
+                "pagedevict::attend(", "pagedevict::rank_tokens", "pagedevict::rank_pages",
+                "pagedevict::score_pages", "pagedevict::memory_bytes", "pagedevict::PolicyConfig::validate"):
+        assert sym in syms, sym
+    deps = subprocess.run(["ldd", str(lib)], capture_output=True, text=True).stdout
+    assert "libpe_b200.so" in deps
+    C.CDLL(str(lib))  # loads without a GPU
