@@ -93,6 +93,9 @@ struct pe_engine {
     int pending[4];                      // slots staged by the current call
     int n_pending = 0;
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t aux_stream = nullptr;   // second prefill wave stream
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_meta = nullptr;       // prefill metadata H2D copies done
     float* part_o = nullptr;
     size_t part_o_elems = 0;
     float* part_ml = nullptr;
@@ -330,7 +333,11 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             return cleanup_fail(fail(PE_CUDA_ERROR, "state initialisation failed"));
         }
     }
-    if (cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&e->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_meta, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
         return cleanup_fail(fail(PE_CUDA_ERROR, "copy stream creation failed"));
     }
@@ -385,6 +392,10 @@ pe_status pe_engine_destroy(pe_engine* e) {
         if (sl.consumed) cudaEventDestroy(sl.consumed);
     }
     if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
+    if (e->aux_stream) cudaStreamDestroy(e->aux_stream);
+    if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+    if (e->ev_join) cudaEventDestroy(e->ev_join);
+    if (e->ev_meta) cudaEventDestroy(e->ev_meta);
     if (e->h_tab_len) cudaFreeHost(e->h_tab_len);
     if (e->h_tab_tok0) cudaFreeHost(e->h_tab_tok0);
     if (e->h_tab_pagebase) cudaFreeHost(e->h_tab_pagebase);
@@ -412,6 +423,9 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     int64_t total_pages = 0;
     int64_t total_keys = 0;
     int max_len = 0;
+    // the pinned per-table arrays are still being copied by the previous call
+    // until its metadata event fires
+    PE_CUDA(cudaEventSynchronize(e->ev_meta));
     for (int q = 0; q < n_seqs; ++q) {
         const int L = cu_seqlens[q + 1] - cu_seqlens[q];
         if (L <= 0) return fail(PE_ERROR, "prefill requires at least one token");  // policy.cpp:57-58
@@ -452,6 +466,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     PE_CUDA(cudaMemcpyAsync(e->tab_tok0, e->h_tab_tok0, sizeof(int64_t) * n_tab, cudaMemcpyHostToDevice, st));
     PE_CUDA(cudaMemcpyAsync(e->tab_pagebase, e->h_tab_pagebase, sizeof(int32_t) * n_tab, cudaMemcpyHostToDevice, st));
     PE_CUDA(cudaMemcpyAsync(e->tab_keybase, e->h_tab_keybase, sizeof(int64_t) * n_tab, cudaMemcpyHostToDevice, st));
+    PE_CUDA(cudaEventRecord(e->ev_meta, st));
     const bool ev_dev = evicted_counts && is_device_ptr(evicted_counts);
     PrefillArgs a{};
     a.k = dk;
@@ -474,21 +489,51 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     a.chunk_cap = use_cta_select ? max_len : chunk_cap;  // keys held in smem per CTA
     if (total_pages > INT32_MAX) return fail(PE_POOL_EXHAUSTED, "page pool exhausted");
     plan_prefill_kernel<<<1, 1024, 0, st>>>(s, a, static_cast<int32_t>(total_pages), e->ctl);
-    launch_prefill_score_any(e->variant, dim3((max_len + kScoreTokensPerCta - 1) / kScoreTokensPerCta, n_seqs), st, s,
-                             a, e->ctl);
-    if (use_cta_select) {
-        // one CTA per table, high key words in shared memory (no cluster barriers)
-        const size_t sel_smem = (((size_t)max_len * 4 + 15) & ~size_t(15)) + kSelHistCopies * 2048 * 4;
-        prefill_select_cta_kernel<<<n_tab, 1024, sel_smem, st>>>(s, a, e->ctl);
-    } else {
-        prefill_select_kernel<<<dim3(kPrefillCluster, n_tab), kPackThreads, pack_smem, st>>>(s, a, e->ctl);
+    // Sequence waves ping-pong between the caller's stream and the engine's
+    // aux stream: while one wave is in its latency-bound select, the other
+    // stream's HBM-bound score / copy kernels keep the memory system busy.
+    // The canonical page reservation (plan) is made once for the whole call.
+    int waves = n_seqs >= 8 ? 4 : (n_seqs >= 2 ? 2 : 1);
+    if (const char* wv = std::getenv("PE_PREFILL_WAVES")) waves = std::max(1, std::min(n_seqs, std::atoi(wv)));
+    if (waves > 1) {
+        PE_CUDA(cudaEventRecord(e->ev_fork, st));
+        PE_CUDA(cudaStreamWaitEvent(e->aux_stream, e->ev_fork, 0));
     }
     const int max_keep_pages = (std::min(max_len, s.policy == PE_POLICY_PAGED_EVICTION ? s.C : max_len) + s.B - 1) / s.B;
-    prefill_copy_kernel<<<dim3((max_keep_pages + 3) / 4, n_tab), 128, 0, st>>>(s, a, e->ctl);
+    for (int w = 0; w < waves; ++w) {
+        const int q0 = (int)((int64_t)n_seqs * w / waves);
+        const int q1 = (int)((int64_t)n_seqs * (w + 1) / waves);
+        if (q1 <= q0) continue;
+        cudaStream_t sw = (w & 1) ? e->aux_stream : st;
+        PrefillArgs aw = a;
+        aw.tab_len += q0 * H;
+        aw.tab_tok0 += q0 * H;
+        aw.tab_pagebase += q0 * H;
+        aw.tab_keybase += q0 * H;
+        if (aw.evicted_counts) aw.evicted_counts += q0 * H;
+        aw.seq_begin = seq_begin + q0;
+        aw.n_tab = (q1 - q0) * H;
+        launch_prefill_score_any(e->variant, dim3((max_len + kScoreTokensPerCta - 1) / kScoreTokensPerCta, q1 - q0),
+                                 sw, s, aw, e->ctl);
+        if (use_cta_select) {
+            // one CTA per table, high key words in shared memory (no cluster barriers)
+            const size_t sel_smem =
+                (((size_t)max_len * 4 + 15) & ~size_t(15)) + kSelHistCopies * 2048 * 4 + kSelCandCap * 4;
+            prefill_select_cta_kernel<<<aw.n_tab, 1024, sel_smem, sw>>>(s, aw, e->ctl);
+        } else {
+            prefill_select_kernel<<<dim3(kPrefillCluster, aw.n_tab), kPackThreads, pack_smem, sw>>>(s, aw, e->ctl);
+        }
+        prefill_copy_kernel<<<dim3((max_keep_pages + 3) / 4, aw.n_tab), 128, 0, sw>>>(s, aw, e->ctl);
+        e->stats.kernel_launches += 3;
+    }
+    if (waves > 1) {
+        PE_CUDA(cudaEventRecord(e->ev_join, e->aux_stream));
+        PE_CUDA(cudaStreamWaitEvent(st, e->ev_join, 0));
+    }
     mark_consumed(e, st);
     r = check_launch(e, "prefill_kernel");
     if (r != PE_OK) return r;
-    e->stats.kernel_launches += 4;
+    e->stats.kernel_launches += 1;
     e->stats.prefill_calls += 1;
     e->stats.tokens_scored += (int64_t)tokens * H;
     if (evicted_counts && !ev_dev) {

@@ -36,7 +36,8 @@ __global__ void plan_prefill_kernel(DevState s, PrefillArgs a, int32_t total_pag
 __global__ void prefill_select_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 __global__ void prefill_select_cta_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 constexpr int kSelHistCopies = 8;        // private histogram copies in the CTA select kernel
-constexpr int kSelectCtaMaxLen = 36864;  // CTA-per-table select: 4 B of smem per token + 64 KB histograms
+constexpr int kSelCandCap = 4096;        // boundary-bin candidates compacted after the first radix pass
+constexpr int kSelectCtaMaxLen = 34816;  // CTA-per-table select: 4 B of smem per token + 64 KB histograms + 16 KB candidates
 __global__ void prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 
 // host-side launchers of the row-geometry-specialised kernels (pe_score.cuh variants)

@@ -501,22 +501,71 @@ __global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s,
     // single histogram would serialise every warp's atomics on them
     uint32_t* hcopy = reinterpret_cast<uint32_t*>(smem + (((size_t)a.chunk_cap * 4 + 15) & ~size_t(15)));
     uint32_t* my_hist = hcopy + ((threadIdx.x >> 5) % kSelHistCopies) * 2048;
+    int32_t* cand = reinterpret_cast<int32_t*>(hcopy + kSelHistCopies * 2048);  // [kSelCandCap]
     const unsigned long long* gk = a.keys + a.tab_keybase[i];
     int32_t* surv = a.surv + (int64_t)a.tab_pagebase[i] * B;
 
-    // ---- 1. high words -> smem, min/max
+    // ---- 0. pivot window from a sorted sample of 1024 high words: every key
+    // whose high word lies in [p_lo, p_hi] is a candidate for the boundary,
+    // the rest are counted as below / above during the load. When the E-th
+    // key falls inside the window (the common case), the radix passes visit
+    // only the candidates; otherwise the plain full-table passes run.
+    const bool sampled = E > 0 && L >= 8192;
+    unsigned int p_lo = 0u, p_hi = 0xFFFFFFFFu;
+    uint32_t* seg = hcopy;  // per-warp candidate segments during the load
+    constexpr int kSegCap = kSelHistCopies * 2048 / 32;
+    if (sampled) {
+        uint32_t* samp = hist;
+        samp[tid] = static_cast<uint32_t>(__ldcg(gk + (int)(((int64_t)tid * L) >> 10)) >> 32);
+        for (int k = 2; k <= 1024; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                __syncthreads();
+                const int o = tid ^ j;
+                if (o > tid) {
+                    const uint32_t x = samp[tid], y = samp[o];
+                    if ((x > y) == ((tid & k) == 0)) {
+                        samp[tid] = y;
+                        samp[o] = x;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        const int r = (int)(((int64_t)E * 1024) / L);
+        const int lo_i = r - 40, hi_i = r + 40;
+        p_lo = lo_i <= 0 ? 0u : samp[lo_i];
+        p_hi = hi_i >= 1023 ? 0xFFFFFFFFu : samp[hi_i];
+        __syncthreads();
+    }
+
+    // ---- 1. high words -> smem, min/max (+ window counts and candidates)
     unsigned int hmin = 0xFFFFFFFFu, hmax = 0u;
-    for (int j0 = tid; j0 < L; j0 += 8 * nthr) {  // 8 independent loads in flight per thread
+    int n_below = 0, seg_n = 0;
+    const int lane_id = tid & 31, warp_id = tid >> 5;
+    for (int j0 = tid - lane_id; j0 < L; j0 += 8 * nthr) {  // 8 independent loads in flight per thread
         unsigned long long kv[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) kv[u] = (j0 + u * nthr < L) ? __ldcs(gk + j0 + u * nthr) : 0ull;
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + lane_id + u * nthr;
+            kv[u] = j < L ? __ldcs(gk + j) : 0ull;
+        }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            if (j0 + u * nthr < L) {
-                const uint32_t w = static_cast<uint32_t>(kv[u] >> 32);
-                hi[j0 + u * nthr] = w;
+            const int j = j0 + lane_id + u * nthr;
+            const bool in = j < L;
+            const uint32_t w = static_cast<uint32_t>(kv[u] >> 32);
+            if (in) {
+                hi[j] = w;
                 hmin = min(hmin, w);
                 hmax = max(hmax, w);
+            }
+            if (sampled) {
+                n_below += in && w < p_lo;
+                const bool c = in && w >= p_lo && w <= p_hi;
+                const unsigned m = __ballot_sync(0xFFFFFFFFu, c);
+                const int at = seg_n + __popc(m & ((1u << lane_id) - 1u));
+                if (c && at < kSegCap) seg[warp_id * kSegCap + at] = j;
+                seg_n += __popc(m);
             }
         }
     }
@@ -524,7 +573,9 @@ __global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s,
     for (int o = 16; o > 0; o >>= 1) {
         hmin = min(hmin, __shfl_xor_sync(0xFFFFFFFFu, hmin, o));
         hmax = max(hmax, __shfl_xor_sync(0xFFFFFFFFu, hmax, o));
+        n_below += __shfl_xor_sync(0xFFFFFFFFu, n_below, o);
     }
+    __shared__ int w_below[32], w_seg[32], win_ok, n_cand;
     if (tid == 0) {
         mm[0] = 0xFFFFFFFFu;
         mm[1] = 0u;
@@ -533,29 +584,68 @@ __global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s,
     if ((tid & 31) == 0) {
         atomicMin(&mm[0], hmin);
         atomicMax(&mm[1], hmax);
+        w_below[warp_id] = n_below;
+        w_seg[warp_id] = seg_n;
     }
     __syncthreads();
+    int below_total = 0;
+    if (sampled) {
+        if (tid == 0) {
+            int b = 0, c = 0, over = 0;
+            for (int w = 0; w < (nthr >> 5); ++w) {
+                b += w_below[w];
+                over |= w_seg[w] > kSegCap;
+                c += w_seg[w];
+            }
+            win_ok = !over && c <= kSelCandCap && b < E && E <= b + c;
+            w_below[0] = b;
+            n_cand = c;
+        }
+        __syncthreads();
+        below_total = w_below[0];
+        if (win_ok) {
+            // contiguous candidate list (warp segments in warp order)
+            int off = 0;
+            for (int w = 0; w < warp_id; ++w) off += w_seg[w];
+            for (int x = lane_id; x < w_seg[warp_id]; x += 32) cand[off + x] = static_cast<int32_t>(seg[warp_id * kSegCap + x]);
+        }
+        __syncthreads();
+    }
+    const bool windowed = sampled && win_ok;
+    if (!windowed) {
+        p_lo = 0u;
+        p_hi = 0xFFFFFFFFu;
+    }
 
     // ---- 2. radix select: threshold key prefix `prefix` of (64 - fshift) bits
     int k_rem = 0;
     int fshift = 64;  // 64: nothing evicted (E == 0)
     unsigned long long prefix = 0;
     if (E > 0) {
-        k_rem = E;
-        const unsigned int gmin = mm[0], gmax = mm[1];
+        k_rem = windowed ? E - below_total : E;
+        // windowed: the candidates' high words lie in [p_lo, p_hi]
+        const unsigned int gmin = windowed ? max(p_lo, mm[0]) : mm[0];
+        const unsigned int gmax = windowed ? min(p_hi, mm[1]) : mm[1];
         const int cpl = (gmin == gmax) ? 32 : __clz(gmin ^ gmax);
         int bitpos = 32 - cpl;  // unresolved bits of the high word
         unsigned int hp = cpl == 0 ? 0u : (cpl == 32 ? gmin : (gmin >> bitpos));
         fshift = 32 + bitpos;
         bool done = false;
+        // Only the keys of the chosen bin can hold the boundary: when they
+        // fit, their indices are compacted into `cand` (after the sample
+        // window, or after the first full pass) and every later pass (high
+        // or low word) visits just them.
+        bool use_cand = windowed;
+        const int n_round_all = (L + nthr - 1) / nthr * nthr;
         while (bitpos > 0) {  // high-word passes (shared memory)
             const int bits = min(11, bitpos);
             const int shift = bitpos - bits;
             const unsigned int dmask = (1u << bits) - 1u;
             for (int b = tid; b < kSelHistCopies * 2048; b += nthr) hcopy[b] = 0;
             __syncthreads();
-            const int n_round = (L + nthr - 1) / nthr * nthr;
-            for (int j = tid; j < n_round; j += nthr) {
+            const int n_iter = use_cand ? (n_cand + nthr - 1) / nthr * nthr : n_round_all;
+            for (int x = tid; x < n_iter; x += nthr) {
+                const int j = use_cand ? (x < n_cand ? cand[x] : L) : x;
                 const unsigned int w = j < L ? hi[j] : 0u;
                 const bool act = j < L && (bitpos == 32 || (w >> bitpos) == hp);
                 hist_add(my_hist, (w >> shift) & dmask, act);
@@ -568,6 +658,20 @@ __global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s,
             bitpos = shift;
             fshift = 32 + shift;
             done = bc[2] == k_rem;
+            if (!done && !use_cand && bc[2] <= kSelCandCap) {
+                // compact the chosen bin (warp-aggregated appends)
+                if (tid == 0) n_cand = 0;
+                __syncthreads();
+                for (int j = tid; j < n_round_all; j += nthr) {
+                    const bool in = j < L && (hi[j] >> bitpos) == hp;
+                    const unsigned m = __ballot_sync(0xFFFFFFFFu, in);
+                    int base = 0;
+                    if ((tid & 31) == 0 && m) base = atomicAdd(&n_cand, __popc(m));
+                    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+                    if (in) cand[base + __popc(m & ((1u << (tid & 31)) - 1u))] = j;
+                }
+                use_cand = true;
+            }
             __syncthreads();
             if (done) break;
         }
@@ -583,8 +687,9 @@ __global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s,
                 const unsigned int dmask = (1u << bits) - 1u;
                 for (int b = tid; b < kSelHistCopies * 2048; b += nthr) hcopy[b] = 0;
                 __syncthreads();
-                const int n_round = (L + nthr - 1) / nthr * nthr;
-                for (int j = tid; j < n_round; j += nthr) {
+                const int n_iter = use_cand ? (n_cand + nthr - 1) / nthr * nthr : n_round_all;
+                for (int x = tid; x < n_iter; x += nthr) {
+                    const int j = use_cand ? (x < n_cand ? cand[x] : L) : x;
                     bool act = j < L && hi[j] == hp;
                     unsigned int lw = 0u;
                     if (act) {
@@ -615,6 +720,10 @@ __global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s,
         less = false;
         tie = false;
         if (E == 0) return;
+        if (hi[j] < p_lo || hi[j] > p_hi) {  // outside the candidate window
+            less = hi[j] < p_lo;
+            return;
+        }
         if (fshift >= 32) {
             const unsigned long long top = static_cast<unsigned long long>(hi[j]) >> (fshift - 32);
             less = top < prefix;

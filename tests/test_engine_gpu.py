@@ -90,6 +90,26 @@ def test_prefill_ties_across_cta_boundaries(select_path):
     np.testing.assert_array_equal(eng.retained_positions(0), np.arange(L - C, L))
 
 
+@pytest.mark.parametrize("gen", [random_kv, grid_kv])
+def test_prefill_long_tables_windowed_select(gen):
+    """Tables of >= 8192 tokens take the sampled pivot window of the CTA
+    select kernel (candidates only; tie-heavy grid data overflows the window
+    and exercises the full-pass fallback). Bit-exact against the oracle."""
+    rng = np.random.default_rng(8192)
+    B, C, d, H = 16, 2048, 128, 2
+    lens = np.array([8192, 32768, 20001, 9000, 4096 + 1])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=len(lens), n_layers=1, H=H, d=d, B=B, C=C, dtype=oracle.BF16)
+    k, _ = gen(rng, (cu[-1], H, d), oracle.BF16)
+    v, _ = gen(rng, (cu[-1], H, d), oracle.BF16)
+    ev = eng.prefill_compress(0, dev(k), dev(v), cu, evicted_counts=True)
+    st, oev = orc.prefill(0, k, v, cu)
+    assert st == 0
+    np.testing.assert_array_equal(ev, oev)
+    eng.sync()
+    check(eng, orc, "windowed: ")
+
+
 @pytest.mark.parametrize("dtype", [oracle.F32, oracle.BF16])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_decode_parity(dtype, mode):
