@@ -21,9 +21,10 @@
 //  * a pool's row width is fixed by the first token appended (or
 //    PoolOptions::row_width): narrower tokens are zero-padded (norms,
 //    scores and dot products are unchanged), wider ones throw LengthMismatch;
-//  * unstructured eviction (BlockTable::evict_slot) and the StreamingLLM /
-//    InvKeyL2 / KeyDiff baselines are not provided by the device engine
-//    (SURVEY §8f-4): they throw pagedevict::Error;
+//  * unstructured eviction (BlockTable::evict_slot, the StreamingLLM /
+//    InvKeyL2 / KeyDiff baselines) marks holes on the device; afterwards
+//    the pool's batched GQA attention (pe_paged_decode_attention) refuses
+//    the engine, attend() here handles holes;
 //  * token positions must be < 2^31 (the device stores int32, D10);
 //  * scores are computed from the token's bytes, not from KvVector's cached
 //    key_norm/value_norm fields (identical for vectors built by make_kv).
@@ -339,6 +340,12 @@ protected:
     static std::vector<std::size_t> device_select_survivors(const std::vector<KvVector>& tokens,
                                                             const PolicyConfig& config);
     static std::int64_t device_paged_evict(BlockTable& table, std::size_t cache_budget);
+    // unstructured eviction of one token by a pe_token_rule; -1 = none
+    static std::int64_t device_token_evict(BlockTable& table, pe_token_rule rule, std::int64_t arg,
+                                           std::size_t cache_budget, std::uint64_t newest_position);
+    // score-based baseline prefill: flags of the k lowest-scoring prompt tokens
+    static std::vector<char> device_prompt_select(const std::vector<KvVector>& tokens, pe_token_rule rule,
+                                                  std::size_t k);
 
     PolicyConfig config_;
 };

@@ -249,6 +249,40 @@ pe_status pe_table_clear(pe_engine* eng, int32_t table, void* stream);
 pe_status pe_table_attend(pe_engine* eng, int32_t table, const float* query, int32_t head_count,
                           int32_t head_dim, float* out, double* weight_sums, void* stream);
 
+/* Unstructured (per-token) eviction of one table: picks a victim among the
+ * retained tokens (logical order) by `rule`, clears its slot and releases
+ * its page once drained (BlockTable::evict_slot, block_table.cpp:33-46).
+ * Rules:
+ *   PE_TOKEN_AT_POSITION   the token at position `arg`; none -> PE_UNKNOWN_POSITION
+ *   PE_TOKEN_STREAMING     oldest token with position >= arg (sink count)  policy.cpp:184-206
+ *   PE_TOKEN_MAX_KEY_NORM  largest ||K||, first on ties                    policy.cpp:219-237
+ *   PE_TOKEN_KEY_DIFF      largest cos(K, mean retained K), first on ties  policy.cpp:263-283
+ * The policy rules skip the token at newest_position and fire only when
+ * retained > cache_budget (cache_budget < 0: unconditional).
+ * *victim_position (nullable) <- evicted position or -1. Needs page_size <= 64;
+ * afterwards pe_paged_decode_attention refuses the engine (holes). */
+typedef enum pe_token_rule {
+    PE_TOKEN_AT_POSITION = 0,
+    PE_TOKEN_STREAMING = 1,
+    PE_TOKEN_MAX_KEY_NORM = 2,
+    PE_TOKEN_KEY_DIFF = 3
+} pe_token_rule;
+pe_status pe_table_evict_token(pe_engine* eng, int32_t table, int32_t rule, int64_t arg, int32_t cache_budget,
+                               int64_t newest_position, int64_t* victim_position, void* stream);
+
+/* Evicted-slot masks (bit s = slot s is a hole) of pages [page_begin, +n_pages). */
+pe_status pe_read_page_holes(pe_engine* eng, int32_t page_begin, int32_t n_pages, uint64_t* holes);
+
+/* Prefill selection of the score-based baselines (compress_by_score,
+ * policy.cpp:90-101): scores every prompt token on `device` —
+ * PE_TOKEN_MAX_KEY_NORM: 1 / max(||K||, 1e-12) (InvKeyL2, policy.cpp:212-216);
+ * PE_TOKEN_KEY_DIFF: -cos(K, mean prompt K) (KeyDiff, policy.cpp:244-260) —
+ * and flags the k lowest (score, position) tokens (rank_tokens,
+ * importance.cpp:41-60). keys: HOST float32 [n][w]; positions: HOST [n];
+ * evicted_flags: HOST [n]. Stateless (no engine). */
+pe_status pe_prompt_select(int32_t device, int32_t rule, const float* keys, int32_t n, int32_t w,
+                           const int64_t* positions, int32_t k, uint8_t* evicted_flags);
+
 /* One table's block-table row (page_ids [num_pages], nullable) and counters. */
 pe_status pe_read_table(pe_engine* eng, int32_t table, int32_t* page_ids, int32_t* num_pages,
                         int32_t* newest_fill, int32_t* retained);

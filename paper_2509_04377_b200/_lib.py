@@ -68,6 +68,9 @@ SIGNATURES = {
     "pe_read_table": (C.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "pe_pool_allocate": (C.c_int, [c_vp, C.POINTER(c_i32)]),
     "pe_pool_release": (C.c_int, [c_vp, c_i32]),
+    "pe_table_evict_token": (C.c_int, [c_vp, c_i32, c_i32, c_i64, c_i32, c_i64, c_vp, c_vp]),
+    "pe_read_page_holes": (C.c_int, [c_vp, c_i32, c_i32, c_vp]),
+    "pe_prompt_select": (C.c_int, [c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_i32, c_vp]),
 }
 
 

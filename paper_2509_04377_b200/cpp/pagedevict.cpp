@@ -197,6 +197,12 @@ struct PagePool::Impl {
         free_slots.push_back(s);
     }
 
+    std::uint64_t holes_of(std::int32_t id) const {
+        std::uint64_t h = 0;
+        if (eng != nullptr) check(pe_read_page_holes(eng, id, 1, &h), "page holes");
+        return h;
+    }
+
     // Refreshes snapshot `id` from the device; `cursor` = slots written.
     Page& snapshot(std::uint32_t id, std::uint32_t cursor) {
         Page& pg = snaps[id];
@@ -209,9 +215,14 @@ struct PagePool::Impl {
         const std::size_t elt = opt.dtype == PE_DTYPE_BF16 ? 2 : 4;
         std::vector<std::uint8_t> bytes(static_cast<std::size_t>(2) * B * info.row_pitch_bytes);
         std::vector<std::int32_t> pos(B);
+        std::uint64_t holes = 0;
         check(pe_read_pages(eng, static_cast<std::int32_t>(id), 1, bytes.data()), "page");
         check(pe_read_positions(eng, static_cast<std::int32_t>(id), 1, pos.data(), nullptr, nullptr), "page");
+        check(pe_read_page_holes(eng, static_cast<std::int32_t>(id), 1, &holes), "page");
+        std::uint32_t fill = 0;
         for (std::uint32_t s = 0; s < cursor; ++s) {
+            if (s < 64 && ((holes >> s) & 1u)) continue;  // evicted slot
+            ++fill;
             const std::uint32_t n = std::min(slot_width[static_cast<std::size_t>(id) * B + s], width);
             KvVector kv;
             kv.key.resize(n);
@@ -232,7 +243,8 @@ struct PagePool::Impl {
             kv.value_norm = l2_norm(kv.value);
             pg.slots_[s] = std::move(kv);
         }
-        pg.cursor_ = pg.fill_ = cursor;
+        pg.cursor_ = cursor;
+        pg.fill_ = fill;
         return pg;
     }
 };
@@ -429,8 +441,19 @@ void BlockTable::free_page(std::size_t logical_index) {
 }
 
 void BlockTable::evict_slot(std::uint64_t position) {
-    (void)position;
-    throw Error("BlockTable::evict_slot: unstructured (per-token) eviction is not provided by the B200 engine");
+    if (slot_ < 0) throw Error("BlockTable was moved from");
+    auto& I = pool_->impl();
+    std::lock_guard lock(I.mu);
+    if (I.eng == nullptr || position > static_cast<std::uint64_t>(std::numeric_limits<std::int32_t>::max()))
+        throw UnknownPosition("no retained token at position " + std::to_string(position));
+    invalidate();
+    const pe_status st = pe_table_evict_token(I.eng, slot_, PE_TOKEN_AT_POSITION, static_cast<std::int64_t>(position),
+                                              -1, -1, nullptr, nullptr);
+    check(st, "BlockTable::evict_slot");
+    const pe_status dev = pe_sync(I.eng);
+    if (dev == PE_UNKNOWN_POSITION)
+        throw UnknownPosition("no retained token at position " + std::to_string(position));
+    if (dev != PE_OK) throw_status(dev, "BlockTable::evict_slot");
 }
 
 std::size_t BlockTable::page_count() const { return view().pages.size(); }
@@ -465,8 +488,13 @@ double BlockTable::fragmentation_ratio() const {
 double BlockTable::fragmentation_ratio_excluding_newest() const {
     const View& v = view();
     if (v.pages.size() <= 1) return 0.0;
+    auto& I = pool_->impl();
+    std::lock_guard lock(I.mu);
+    const std::uint64_t h = I.holes_of(v.pages.back());
+    std::int32_t newest_fill = 0;
+    for (std::int32_t k = 0; k < v.newest_fill; ++k) newest_fill += (k >= 64 || !((h >> k) & 1u));
     const double slots = static_cast<double>(v.pages.size() - 1) * pool_->page_size();
-    return 1.0 - static_cast<double>(v.retained - v.newest_fill) / slots;
+    return 1.0 - static_cast<double>(v.retained - newest_fill) / slots;
 }
 
 std::vector<std::uint64_t> BlockTable::retained_positions() const {
@@ -479,8 +507,10 @@ std::vector<std::uint64_t> BlockTable::retained_positions() const {
     std::vector<std::int32_t> pos(I.B);
     for (std::size_t j = 0; j < v.pages.size(); ++j) {
         check(pe_read_positions(I.eng, v.pages[j], 1, pos.data(), nullptr, nullptr), "retained_positions");
+        const std::uint64_t h = I.holes_of(v.pages[j]);
         const std::uint32_t cur = j + 1 == v.pages.size() ? static_cast<std::uint32_t>(v.newest_fill) : I.B;
-        for (std::uint32_t s = 0; s < cur; ++s) out.push_back(static_cast<std::uint64_t>(pos[s]));
+        for (std::uint32_t s = 0; s < cur; ++s)
+            if (s >= 64 || !((h >> s) & 1u)) out.push_back(static_cast<std::uint64_t>(pos[s]));
     }
     return out;
 }
@@ -705,7 +735,102 @@ std::int64_t EvictionPolicy::device_paged_evict(BlockTable& table, std::size_t c
     return victim;
 }
 
+std::int64_t EvictionPolicy::device_token_evict(BlockTable& table, pe_token_rule rule, std::int64_t arg,
+                                                std::size_t cache_budget, std::uint64_t newest_position) {
+    if (table.slot_ < 0) throw Error("BlockTable was moved from");
+    auto& I = table.pool().impl();
+    std::lock_guard lock(I.mu);
+    if (I.eng == nullptr) return -1;
+    if (cache_budget > static_cast<std::size_t>(std::numeric_limits<std::int32_t>::max()))
+        throw Overflow("budget exceeds int32");
+    std::int64_t victim = -1;
+    table.invalidate();
+    const std::int64_t newest = newest_position > static_cast<std::uint64_t>(std::numeric_limits<std::int64_t>::max())
+                                    ? -1
+                                    : static_cast<std::int64_t>(newest_position);
+    check_sync(I.eng,
+               pe_table_evict_token(I.eng, table.slot_, rule, arg, static_cast<std::int32_t>(cache_budget), newest,
+                                    &victim, nullptr),
+               "decode_step");
+    return victim;
+}
+
+std::vector<char> EvictionPolicy::device_prompt_select(const std::vector<KvVector>& tokens, pe_token_rule rule,
+                                                       std::size_t k) {
+    std::uint32_t W = 0;
+    for (const auto& kv : tokens) W = std::max<std::uint32_t>(W, static_cast<std::uint32_t>(kv.key.size()));
+    const std::size_t n = tokens.size();
+    std::vector<float> K(n * W, 0.0f);
+    std::vector<std::int64_t> pos(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        std::copy(tokens[i].key.begin(), tokens[i].key.end(), K.begin() + static_cast<std::ptrdiff_t>(i * W));
+        pos[i] = checked_position(tokens[i].position);
+    }
+    std::vector<std::uint8_t> flags(n, 0);
+    check(pe_prompt_select(0, rule, K.data(), static_cast<std::int32_t>(n), static_cast<std::int32_t>(W), pos.data(),
+                           static_cast<std::int32_t>(k), flags.data()),
+          "prefill_compress");
+    return std::vector<char>(flags.begin(), flags.end());
+}
+
 namespace {
+
+// Splits the prompt by eviction flags: survivors in input order, evicted
+// positions ascending (drop_positions / rank_tokens, policy.cpp:75-101).
+PrefillResult split_by_flags(std::vector<KvVector> tokens, const std::vector<char>& evict) {
+    std::vector<std::uint64_t> evicted;
+    std::vector<KvVector> retained;
+    for (std::size_t i = 0; i < tokens.size(); ++i) {
+        if (evict[i]) evicted.push_back(tokens[i].position);
+        else retained.push_back(std::move(tokens[i]));
+    }
+    std::sort(evicted.begin(), evicted.end());
+    return PrefillResult{std::move(retained), EvictionDecision::tokens(std::move(evicted), 0)};
+}
+
+// StreamingLLM (policy.cpp:158-207): prefill keeps the sinks and the recent
+// window by index; decode evicts the oldest non-sink token on the device.
+class DeviceStreamingLlm final : public EvictionPolicy {
+public:
+    using EvictionPolicy::EvictionPolicy;
+
+protected:
+    PrefillResult compress(std::vector<KvVector> tokens) const override {
+        const std::size_t sinks = std::min(config_.sink_count, tokens.size());
+        const std::size_t window_start = tokens.size() - (config_.cache_budget - sinks);
+        std::vector<char> evict(tokens.size(), 0);
+        for (std::size_t i = sinks; i < window_start; ++i) evict[i] = 1;
+        return split_by_flags(std::move(tokens), evict);
+    }
+    EvictionDecision evict(BlockTable& table, std::uint64_t newest, std::int64_t step) override {
+        const std::int64_t v = device_token_evict(table, PE_TOKEN_STREAMING,
+                                                  static_cast<std::int64_t>(config_.sink_count),
+                                                  config_.cache_budget, newest);
+        if (v < 0) return EvictionDecision::none(step);
+        return EvictionDecision::tokens({static_cast<std::uint64_t>(v)}, step);
+    }
+};
+
+// InvKeyL2 / KeyDiff (policy.cpp:209-284): score-based prefill and a
+// per-step token eviction, both scored on the device.
+class DeviceScoredTokenPolicy final : public EvictionPolicy {
+public:
+    DeviceScoredTokenPolicy(PolicyConfig c, pe_token_rule rule) : EvictionPolicy(c), rule_(rule) {}
+
+protected:
+    PrefillResult compress(std::vector<KvVector> tokens) const override {
+        const auto evict = device_prompt_select(tokens, rule_, tokens.size() - config_.cache_budget);
+        return split_by_flags(std::move(tokens), evict);
+    }
+    EvictionDecision evict(BlockTable& table, std::uint64_t newest, std::int64_t step) override {
+        const std::int64_t v = device_token_evict(table, rule_, 0, config_.cache_budget, newest);
+        if (v < 0) return EvictionDecision::none(step);
+        return EvictionDecision::tokens({static_cast<std::uint64_t>(v)}, step);
+    }
+
+private:
+    pe_token_rule rule_;
+};
 
 class DevicePagedEviction final : public EvictionPolicy {
 public:
@@ -754,12 +879,9 @@ std::unique_ptr<EvictionPolicy> make_policy(PolicyConfig config) {
     switch (config.kind) {
     case PolicyKind::PagedEviction: return std::make_unique<DevicePagedEviction>(config);
     case PolicyKind::FullCache: return std::make_unique<DeviceFullCache>(config);
-    case PolicyKind::StreamingLlm:
-    case PolicyKind::InvKeyL2:
-    case PolicyKind::KeyDiff:
-        config.validate();
-        throw Error("policy '" + std::string(to_string(config.kind)) +
-                    "' is not provided by the B200 engine (unstructured baselines are out of scope)");
+    case PolicyKind::StreamingLlm: return std::make_unique<DeviceStreamingLlm>(config);
+    case PolicyKind::InvKeyL2: return std::make_unique<DeviceScoredTokenPolicy>(config, PE_TOKEN_MAX_KEY_NORM);
+    case PolicyKind::KeyDiff: return std::make_unique<DeviceScoredTokenPolicy>(config, PE_TOKEN_KEY_DIFF);
     }
     throw Error("unknown policy kind");
 }

@@ -154,11 +154,16 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
         s.newest_fill[t] = slot + 1;
         s.retained[t] += 1;
         if (slot + 1 == s.B) {
-            // page_score, importance.cpp:19-30: mean over the B slots in slot order
+            // page_score, importance.cpp:19-30: mean over the occupied slots in slot order
             double sum = 0.0;
-            for (int j = 0; j < s.B - 1; ++j) sum += s.token_scores[(int64_t)page * s.B + j];
+            int cnt = 1;
+            for (int j = 0; j < s.B - 1; ++j) {
+                if (slot_hole(s, page, j)) continue;
+                sum += s.token_scores[(int64_t)page * s.B + j];
+                ++cnt;
+            }
             sum += S;
-            s.page_scores[page] = sum / static_cast<double>(s.B);
+            s.page_scores[page] = sum / static_cast<double>(cnt);
         }
     }
     (void)nw;
@@ -204,7 +209,10 @@ __device__ __forceinline__ void finalize_evict(const DevState& s, int t, int i, 
     if (lane == 0) {
         row[N - 1] = -1;
         s.num_pages[t] = N - 1;
-        s.retained[t] -= s.B;  // every page is full when the trigger fires
+        // every page is write-full when the trigger fires; holes only come
+        // from the table API's unstructured eviction
+        s.retained[t] -= page_fill(s, victim_page, s.B);
+        if (s.holes_on) s.holes[victim_page] = 0ull;
         s.newest_fill[t] = (N - 1 > 0) ? s.B : 0;
         vpage[i] = victim_page;
         if (victims) victims[i] = victim;
@@ -295,18 +303,33 @@ __global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
             const int slot = lane >> 1;
             const int64_t ko = (int64_t)slot * s.pitch, vo = (int64_t)(16 + slot) * s.pitch;
             for (int lp = wid; lp < np; lp += nw) {
-                const uint8_t* base = s.pages + (int64_t)__ldg(row + p0 + lp) * page_bytes;
+                const int id = __ldg(row + p0 + lp);
+                const uint8_t* base = s.pages + (int64_t)id * page_bytes;
                 const double S = pair_token_score<SV>(base + ko, base + vo, true, s.w, s.dtype);
                 double sum = 0.0;
+                if (!s.holes_on) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
-                if (lane == 0) page_mean[lp] = sum / 16.0;
+                    for (int j = 0; j < 16; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+                    if (lane == 0) page_mean[lp] = sum / 16.0;
+                } else {  // mean over the occupied slots (page_score, importance.cpp:19-30)
+                    const unsigned long long hm = s.holes[id];
+                    int cnt = 0;
+                    for (int j = 0; j < 16; ++j) {
+                        const double x = __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+                        if (!((hm >> j) & 1ull)) {
+                            sum += x;
+                            ++cnt;
+                        }
+                    }
+                    if (lane == 0) page_mean[lp] = sum / static_cast<double>(cnt);
+                }
             }
         } else {
             for (int lp = wid; lp < np; lp += nw) {
                 const int id = __ldg(row + p0 + lp);
                 const uint8_t* base = s.pages + (int64_t)id * page_bytes;
                 double sum = 0.0;
+                int cnt = 0;
                 for (int s0 = 0; s0 < s.B; s0 += 16) {
                     const int slot = s0 + (lane >> 1);
                     const bool valid = slot < s.B;
@@ -314,9 +337,15 @@ __global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
                                                           base + (int64_t)(s.B + slot) * s.pitch, valid, s.w,
                                                           s.dtype);
                     const int ns = min(16, s.B - s0);
-                    for (int j = 0; j < ns; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+                    for (int j = 0; j < ns; ++j) {
+                        const double x = __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+                        if (!slot_hole(s, id, s0 + j)) {
+                            sum += x;
+                            ++cnt;
+                        }
+                    }
                 }
-                if (lane == 0) page_mean[lp] = sum / static_cast<double>(s.B);
+                if (lane == 0) page_mean[lp] = sum / static_cast<double>(cnt);
             }
         }
         __syncthreads();

@@ -106,6 +106,7 @@ struct pe_engine {
     int max_dyn_prefill = 0, max_dyn_attn = 0;
     // table-granular API (pe_table_*, pe_pool_*)
     int32_t* alloc_out = nullptr;
+    int64_t* tok_out = nullptr;
     double* attend_logits = nullptr;
     size_t attend_logits_elems = 0;
     float* attend_out = nullptr;
@@ -287,8 +288,9 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         dalloc(&s.retained, n_tables) != cudaSuccess || dalloc(&s.stack, (size_t)cap) != cudaSuccess ||
         dalloc(&s.top, 1) != cudaSuccess || dalloc(&s.status, 1) != cudaSuccess ||
         dalloc(&s.evict_count, 1) != cudaSuccess || dalloc(&s.grid_ctr, 1) != cudaSuccess ||
+        dalloc(&s.holes, (size_t)cap) != cudaSuccess ||
         dalloc(&e->vpage, n_tables) != cudaSuccess || dalloc(&e->ctl, 1) != cudaSuccess ||
-        dalloc(&e->alloc_out, 1) != cudaSuccess ||
+        dalloc(&e->alloc_out, 1) != cudaSuccess || dalloc(&e->tok_out, 1) != cudaSuccess ||
         dalloc(&e->lb_status, (size_t)n_tables / 64 + 2) != cudaSuccess ||
         dalloc(&e->rank, n_tables) != cudaSuccess || dalloc(&e->work, n_tables) != cudaSuccess ||
         dalloc(&e->victims, n_tables) != cudaSuccess || dalloc(&e->tickets, n_tables) != cudaSuccess ||
@@ -327,6 +329,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             cudaMemset(e->lb_status, 0, sizeof(unsigned long long) * ((size_t)n_tables / 64 + 2)) != cudaSuccess ||
             cudaMemset(e->ctl, 0, sizeof(LaunchCtl)) != cudaSuccess ||
             cudaMemset(s.positions, 0xFF, sizeof(int32_t) * (size_t)cap * s.B) != cudaSuccess ||
+            cudaMemset(s.holes, 0, sizeof(unsigned long long) * (size_t)cap) != cudaSuccess ||
             cudaMemset(s.pages, 0, (size_t)cap * page_bytes) != cudaSuccess ||
             cudaDeviceSynchronize() != cudaSuccess) {
             cudaGetLastError();
@@ -376,13 +379,13 @@ pe_status pe_engine_destroy(pe_engine* e) {
     cudaSetDevice(e->device);
     cudaDeviceSynchronize();
     DevState& s = e->s;
-    void* dev[] = {s.pages, s.positions, s.token_scores, s.page_scores, s.block_table, s.num_pages,
+    void* dev[] = {s.holes, s.pages, s.positions, s.token_scores, s.page_scores, s.block_table, s.num_pages,
                    s.newest_fill, s.retained, s.stack, s.top, s.status, s.evict_count, s.grid_ctr, e->vpage,
                    e->ctl, e->rank,
                    e->work, e->victims, e->tickets, e->evict_scratch, e->tab_len, e->tab_tok0,
                    e->tab_pagebase, e->evicted_dev, e->part_o,
                    e->part_ml, e->out_stage, e->tab_keybase, e->keys, e->surv, e->lb_status,
-                   e->alloc_out, e->attend_logits, e->attend_out, e->attend_ws};
+                   e->alloc_out, e->tok_out, e->attend_logits, e->attend_out, e->attend_ws};
     for (void* p : dev) {
         if (p) cudaFree(p);
     }
@@ -653,6 +656,8 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
     const DevState& s = e->s;
     if (e->cfg.granularity != PE_GRANULARITY_PER_KV_HEAD)
         return fail(PE_INVALID_ARG, "attention requires PER_KV_HEAD tables");
+    if (s.holes_on)
+        return fail(PE_INVALID_STATE, "tables with evicted slots (unstructured eviction): use pe_table_attend");
     if (layer < 0 || layer >= s.n_layers) return fail(PE_INVALID_ARG, "layer out of range");
     if (n_q_heads <= 0 || n_q_heads % s.tab_heads != 0)
         return fail(PE_LENGTH_MISMATCH, "query heads must be a multiple of KV heads");
@@ -928,15 +933,16 @@ pe_status pe_table_attend(pe_engine* e, int32_t table, const float* query, int32
         return fail(PE_LENGTH_MISMATCH, "head_count * head_dim exceeds the pool row width");
     cudaSetDevice(e->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    int32_t R = 0;
+    int32_t R = 0, NP = 0;
     PE_CUDA(cudaStreamSynchronize(st));
     PE_CUDA(cudaMemcpy(&R, s.retained + table, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    PE_CUDA(cudaMemcpy(&NP, s.num_pages + table, sizeof(int32_t), cudaMemcpyDeviceToHost));
     if (R <= 0) return fail(PE_EMPTY_CACHE, "attention requires at least one retained token");
     const size_t width = (size_t)head_count * head_dim;
     e->n_pending = 0;
     const uint8_t* dq = nullptr;
     if ((r = as_device(e, query, sizeof(float) * width, st, &dq)) != PE_OK) return r;
-    if ((r = ensure_t(&e->attend_logits, &e->attend_logits_elems, (size_t)R * head_count)) != PE_OK) return r;
+    if ((r = ensure_t(&e->attend_logits, &e->attend_logits_elems, (size_t)NP * s.B * head_count)) != PE_OK) return r;
     if ((r = ensure_t(&e->attend_out, &e->attend_out_elems, width)) != PE_OK) return r;
     if ((r = ensure_t(&e->attend_ws, &e->attend_ws_elems, (size_t)head_count)) != PE_OK) return r;
     const bool out_dev = is_device_ptr(out);
@@ -972,6 +978,37 @@ pe_status pe_read_table(pe_engine* e, int32_t table, int32_t* page_ids, int32_t*
     return PE_OK;
 }
 
+pe_status pe_table_evict_token(pe_engine* e, int32_t table, int32_t rule, int64_t arg, int32_t cache_budget,
+                               int64_t newest_position, int64_t* victim_position, void* stream) {
+    pe_status r = check_table(e, table);
+    if (r != PE_OK) return r;
+    if (rule < PE_TOKEN_AT_POSITION || rule > PE_TOKEN_KEY_DIFF) return fail(PE_INVALID_ARG, "token rule");
+    if (e->s.B > 64) return fail(PE_INVALID_ARG, "unstructured eviction needs page_size <= 64");
+    cudaSetDevice(e->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    e->s.holes_on = 1;  // from now on every kernel honours the hole masks
+    if ((r = ensure_t(&e->attend_out, &e->attend_out_elems, (size_t)e->s.w)) != PE_OK) return r;
+    token_evict_kernel<<<1, 256, 0, st>>>(e->s, table, rule, static_cast<long long>(arg), cache_budget,
+                                          static_cast<long long>(newest_position), e->attend_out,
+                                          reinterpret_cast<long long*>(e->tok_out));
+    if ((r = check_launch(e, "token_evict_kernel")) != PE_OK) return r;
+    e->stats.kernel_launches += 1;
+    if (victim_position != nullptr)
+        PE_CUDA(cudaMemcpyAsync(victim_position, e->tok_out, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    return PE_OK;
+}
+
+pe_status pe_read_page_holes(pe_engine* e, int32_t page_begin, int32_t n_pages, uint64_t* holes) {
+    if (e == nullptr || holes == nullptr) return fail(PE_INVALID_ARG, "null argument");
+    const DevState& s = e->s;
+    if (page_begin < 0 || n_pages < 0 || page_begin + n_pages > s.capacity)
+        return fail(PE_INDEX_OUT_OF_RANGE, "page range out of range");
+    cudaSetDevice(e->device);
+    PE_CUDA(cudaDeviceSynchronize());
+    PE_CUDA(cudaMemcpy(holes, s.holes + page_begin, sizeof(uint64_t) * n_pages, cudaMemcpyDeviceToHost));
+    return PE_OK;
+}
+
 pe_status pe_pool_allocate(pe_engine* e, int32_t* page_id) {
     if (e == nullptr || page_id == nullptr) return fail(PE_INVALID_ARG, "null argument");
     cudaSetDevice(e->device);
@@ -993,6 +1030,61 @@ pe_status pe_pool_release(pe_engine* e, int32_t page_id) {
     if (r != PE_OK) return r;
     e->stats.kernel_launches += 1;
     return pe_sync(e);
+}
+
+// ------------------------------------------------------------------ baseline prefill selection
+pe_status pe_prompt_select(int32_t device, int32_t rule, const float* keys, int32_t n, int32_t w,
+                           const int64_t* positions, int32_t k, uint8_t* evicted_flags) {
+    if (rule != PE_TOKEN_MAX_KEY_NORM && rule != PE_TOKEN_KEY_DIFF) return fail(PE_INVALID_ARG, "prompt rule");
+    if (keys == nullptr || positions == nullptr || evicted_flags == nullptr) return fail(PE_INVALID_ARG, "null buffer");
+    if (n <= 0 || w <= 0) return fail(PE_EMPTY_INPUT, "empty prompt");
+    if (k < 0 || k > n) return fail(PE_K_TOO_LARGE, "k exceeds the scored tokens");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(PE_NO_DEVICE, "no CUDA device");
+    }
+    if (device < 0 || device >= ndev) return fail(PE_NO_DEVICE, "device ordinal out of range");
+    PE_CUDA(cudaSetDevice(device));
+    int n_pad = 1;
+    while (n_pad < n) n_pad <<= 1;
+    float *dk = nullptr, *mean = nullptr;
+    double *score = nullptr, *mnorm = nullptr;
+    long long *pos = nullptr, *spos = nullptr;
+    int* sidx = nullptr;
+    uint8_t* flags = nullptr;
+    auto release = [&]() {
+        void* ps[] = {dk, mean, score, mnorm, pos, spos, sidx, flags};
+        for (void* p : ps)
+            if (p) cudaFree(p);
+    };
+    if (dalloc(&dk, (size_t)n * w) != cudaSuccess || dalloc(&mean, (size_t)w) != cudaSuccess ||
+        dalloc(&score, (size_t)n_pad) != cudaSuccess || dalloc(&mnorm, 1) != cudaSuccess ||
+        dalloc(&pos, (size_t)n) != cudaSuccess || dalloc(&spos, (size_t)n_pad) != cudaSuccess ||
+        dalloc(&sidx, (size_t)n_pad) != cudaSuccess || dalloc(&flags, (size_t)n) != cudaSuccess) {
+        cudaGetLastError();
+        release();
+        return fail(PE_CUDA_ERROR, "device allocation failed");
+    }
+    cudaError_t ce = cudaMemcpy(dk, keys, sizeof(float) * (size_t)n * w, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMemcpy(pos, positions, sizeof(int64_t) * n, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMemset(flags, 0, n);
+    if (ce == cudaSuccess && rule == PE_TOKEN_KEY_DIFF) {
+        prompt_mean_key_kernel<<<1, 256>>>(dk, n, w, mean, mnorm);
+        ce = cudaGetLastError();
+    }
+    if (ce == cudaSuccess) {
+        prompt_score_kernel<<<(n_pad + 255) / 256, 256>>>(dk, n, w, rule, mean, mnorm, pos, n_pad, score, spos, sidx);
+        for (int kk = 2; kk <= n_pad; kk <<= 1)
+            for (int j = kk >> 1; j > 0; j >>= 1)
+                bitonic_step_kernel<<<(n_pad + 255) / 256, 256>>>(score, spos, sidx, n_pad, j, kk);
+        if (k > 0) flag_first_kernel<<<(k + 255) / 256, 256>>>(sidx, k, flags);
+        ce = cudaGetLastError();
+    }
+    if (ce == cudaSuccess) ce = cudaMemcpy(evicted_flags, flags, (size_t)n, cudaMemcpyDeviceToHost);
+    release();
+    if (ce != cudaSuccess) return fail(PE_CUDA_ERROR, std::string("prompt select: ") + cudaGetErrorString(ce));
+    return PE_OK;
 }
 
 }  // extern "C"

@@ -33,9 +33,25 @@ struct DevState {
     int32_t* status;
     unsigned long long* evict_count;
     unsigned long long* grid_ctr;   // monotonically increasing CTA completion tickets
+    // Unstructured (per-token) eviction, table API only: bit s of holes[p]
+    // marks an evicted slot of page p (Page::evict, page.hpp:47-56); cleared
+    // when the page is released. holes_on = 0 until the first hole is made,
+    // so the PagedEviction kernels never read the array before that.
+    unsigned long long* holes;      // [capacity]
+    int32_t holes_on;
     int32_t capacity, B, C, w, pitch, row_bytes, max_pages, n_tables;
     int32_t n_seqs, n_layers, tab_heads, dtype, policy;
 };
+
+// Occupied-slot count of a page whose first `cursor` slots were written.
+__device__ __forceinline__ int page_fill(const DevState& s, int page, int cursor) {
+    if (!s.holes_on) return cursor;
+    const unsigned long long m = cursor >= 64 ? ~0ull : ((1ull << cursor) - 1ull);
+    return cursor - __popcll(s.holes[page] & m);
+}
+__device__ __forceinline__ bool slot_hole(const DevState& s, int page, int slot) {
+    return s.holes_on && slot < 64 && ((s.holes[page] >> slot) & 1ull);
+}
 
 // Per-launch control block written by the plan kernels.
 struct LaunchCtl {

@@ -72,5 +72,12 @@ __global__ void table_free_page_kernel(DevState s, int32_t t, int32_t idx);
 __global__ void table_clear_kernel(DevState s, int32_t t);
 __global__ void table_attend_kernel(DevState s, int32_t t, const float* q, int32_t head_dim, double* logits,
                                     float* out, double* weight_sums);
+__global__ void token_evict_kernel(DevState s, int32_t t, int32_t rule, long long arg, int32_t C, long long newest,
+                                   float* mean, long long* out);
+__global__ void prompt_mean_key_kernel(const float* k, int n, int w, float* mean, double* mnorm);
+__global__ void prompt_score_kernel(const float* k, int n, int w, int rule, const float* mean, const double* mnorm,
+                                    const long long* pos, int n_pad, double* score, long long* spos, int* sidx);
+__global__ void bitonic_step_kernel(double* score, long long* spos, int* sidx, int n_pad, int j, int k);
+__global__ void flag_first_kernel(const int* sidx, int k, uint8_t* flags);
 
 }  // namespace pe

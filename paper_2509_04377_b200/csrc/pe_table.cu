@@ -22,6 +22,7 @@ __global__ void pool_allocate_kernel(DevState s, int32_t* out) {
     }
     const int id = s.stack[top - 1];
     *s.top = top - 1;
+    s.holes[id] = 0ull;  // Page::reset (page_pool.cpp:31)
     *out = id;
 }
 
@@ -33,6 +34,7 @@ __global__ void pool_release_kernel(DevState s, int32_t id) {
     }
     s.stack[top] = id;
     *s.top = top + 1;
+    s.holes[id] = 0ull;
 }
 
 // One warp. Every non-newest page is full (the engine never leaves holes),
@@ -46,7 +48,7 @@ __global__ void table_free_page_kernel(DevState s, int32_t t, int32_t idx) {
     }
     int32_t* row = s.block_table + (int64_t)t * s.max_pages;
     const int page = row[idx];
-    const int fill = (idx == N - 1) ? s.newest_fill[t] : s.B;
+    const int fill = page_fill(s, page, (idx == N - 1) ? s.newest_fill[t] : s.B);
     for (int base = idx; base < N - 1; base += 32) {
         const int v = (base + lane + 1 < N) ? row[base + lane + 1] : 0;
         __syncwarp();
@@ -58,6 +60,7 @@ __global__ void table_free_page_kernel(DevState s, int32_t t, int32_t idx) {
         s.num_pages[t] = N - 1;
         s.retained[t] -= fill;
         if (idx == N - 1) s.newest_fill[t] = (N - 1 > 0) ? s.B : 0;
+        s.holes[page] = 0ull;
         const int top = *s.top;
         s.stack[top] = page;
         *s.top = top + 1;
@@ -71,6 +74,7 @@ __global__ void table_clear_kernel(DevState s, int32_t t) {
     const int top = *s.top;
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
         s.stack[top + j] = row[j];
+        s.holes[row[j]] = 0ull;
         row[j] = -1;
     }
     __syncthreads();
@@ -100,25 +104,30 @@ __global__ void table_attend_kernel(DevState s, int32_t t, const float* __restri
                                     double* logits, float* out, double* weight_sums) {
     const int h = blockIdx.x;
     const int N = s.num_pages[t];
-    const int R = s.retained[t];
+    const int nf = s.newest_fill[t];
+    const int X = N * s.B;  // slot index x = logical page * B + slot; holes and unwritten slots skipped
     const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
     const int64_t page_bytes = (int64_t)2 * s.B * s.pitch;
     const int64_t elt = s.dtype == PE_DTYPE_BF16 ? 2 : 4;
     const float* qh = q + (int64_t)h * head_dim;
-    double* lg = logits + (int64_t)h * R;
+    double* lg = logits + (int64_t)h * X;
     const double scale = 1.0 / sqrt(static_cast<double>(head_dim));
-    (void)N;
+    auto valid = [&](int x) {
+        const int j = x / s.B, sl = x % s.B;
+        return sl < (j == N - 1 ? nf : s.B) && !slot_hole(s, row[j], sl);
+    };
     __shared__ double red[32];
     __shared__ double sh_max, sh_sum;
     // pass 1: logits
     double mx = -INFINITY;
-    for (int i = threadIdx.x; i < R; i += blockDim.x) {
-        const uint8_t* krow = s.pages + (int64_t)row[i / s.B] * page_bytes + (int64_t)(i % s.B) * s.pitch +
+    for (int x = threadIdx.x; x < X; x += blockDim.x) {
+        if (!valid(x)) continue;
+        const uint8_t* krow = s.pages + (int64_t)row[x / s.B] * page_bytes + (int64_t)(x % s.B) * s.pitch +
                               (int64_t)h * head_dim * elt;
         double dot = 0.0;
         for (int j = 0; j < head_dim; ++j) dot = fma(static_cast<double>(qh[j]), row_elem(krow, j, s.dtype), dot);
         const double l = __dmul_rn(dot, scale);
-        lg[i] = l;
+        lg[x] = l;
         mx = fmax(mx, l);
     }
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
@@ -131,11 +140,13 @@ __global__ void table_attend_kernel(DevState s, int32_t t, const float* __restri
     }
     __syncthreads();
     const double m = sh_max;
-    for (int i = threadIdx.x; i < R; i += blockDim.x) lg[i] = exp(lg[i] - m);
+    for (int x = threadIdx.x; x < X; x += blockDim.x)
+        if (valid(x)) lg[x] = exp(lg[x] - m);
     __syncthreads();
     if (threadIdx.x == 0) {  // sequential in logical order, as the reference
         double sum = 0.0;
-        for (int i = 0; i < R; ++i) sum = __dadd_rn(sum, lg[i]);
+        for (int x = 0; x < X; ++x)
+            if (valid(x)) sum = __dadd_rn(sum, lg[x]);
         sh_sum = sum;
     }
     __syncthreads();
@@ -143,19 +154,235 @@ __global__ void table_attend_kernel(DevState s, int32_t t, const float* __restri
     // pass 2: one accumulator per output element, tokens in logical order
     for (int j = threadIdx.x; j < head_dim; j += blockDim.x) {
         double acc = 0.0;
-        for (int i = 0; i < R; ++i) {
-            const uint8_t* vrow = s.pages + (int64_t)row[i / s.B] * page_bytes +
-                                  (int64_t)(s.B + i % s.B) * s.pitch + (int64_t)h * head_dim * elt;
-            const double w = __ddiv_rn(lg[i], ws);
+        for (int x = 0; x < X; ++x) {
+            if (!valid(x)) continue;
+            const uint8_t* vrow = s.pages + (int64_t)row[x / s.B] * page_bytes +
+                                  (int64_t)(s.B + x % s.B) * s.pitch + (int64_t)h * head_dim * elt;
+            const double w = __ddiv_rn(lg[x], ws);
             acc = __dadd_rn(acc, __dmul_rn(w, row_elem(vrow, j, s.dtype)));
         }
         out[(int64_t)h * head_dim + j] = static_cast<float>(acc);
     }
     if (weight_sums != nullptr && threadIdx.x == 0) {
         double tot = 0.0;
-        for (int i = 0; i < R; ++i) tot = __dadd_rn(tot, __ddiv_rn(lg[i], ws));
+        for (int x = 0; x < X; ++x)
+            if (valid(x)) tot = __dadd_rn(tot, __ddiv_rn(lg[x], ws));
         weight_sums[h] = tot;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Unstructured (per-token) eviction of one table (one CTA): picks a victim
+// by `rule` among the retained tokens in logical order, then clears its slot
+// (Page::evict, page.hpp:47-56) and auto-frees the page once it drains
+// (BlockTable::evict_slot, block_table.cpp:33-46).
+//   PE_TOKEN_AT_POSITION   the token at position `arg`          (evict_slot)
+//   PE_TOKEN_STREAMING     oldest token with position >= arg    (StreamingLlmPolicy::evict, policy.cpp:184-206)
+//   PE_TOKEN_MAX_KEY_NORM  largest ||K||, first on ties         (InvKeyL2Policy::evict, policy.cpp:219-237)
+//   PE_TOKEN_KEY_DIFF      largest cos(K, mean K), first on ties (KeyDiffPolicy::evict, policy.cpp:263-283)
+// The policies skip the step's own token (`newest`) and fire only when
+// retained > C (C < 0: unconditional). *out = victim position or -1.
+__device__ __forceinline__ double row_sumsq_f(const uint8_t* row, int w, int dtype) {
+    double acc = 0.0;
+    for (int i = 0; i < w; ++i) {
+        const double x = row_elem(row, i, dtype);
+        acc = fma(x, x, acc);
+    }
+    return acc;
+}
+
+__global__ void token_evict_kernel(DevState s, int32_t t, int32_t rule, long long arg, int32_t C, long long newest,
+                                   float* mean, long long* out) {
+    __shared__ double sh_val[256];
+    __shared__ int sh_x[256];
+    __shared__ double sh_mnorm;
+    const int N = s.num_pages[t];
+    const int nf = s.newest_fill[t];
+    const int X = N * s.B;
+    int32_t* row = s.block_table + (int64_t)t * s.max_pages;
+    const int64_t page_bytes = (int64_t)2 * s.B * s.pitch;
+    if (C >= 0 && s.retained[t] <= C) {
+        if (threadIdx.x == 0) *out = -1;
+        return;
+    }
+    auto valid = [&](int x) {
+        const int j = x / s.B, sl = x % s.B;
+        return sl < (j == N - 1 ? nf : s.B) && !slot_hole(s, row[j], sl);
+    };
+    auto krow = [&](int x) { return s.pages + (int64_t)row[x / s.B] * page_bytes + (int64_t)(x % s.B) * s.pitch; };
+    auto pos_of = [&](int x) { return (long long)s.positions[(int64_t)row[x / s.B] * s.B + x % s.B]; };
+    if (rule == PE_TOKEN_KEY_DIFF) {
+        // mean_key (policy.cpp:117-134): double sums in logical order, cast to float
+        for (int i = threadIdx.x; i < s.w; i += blockDim.x) {
+            double acc = 0.0;
+            int cnt = 0;
+            for (int x = 0; x < X; ++x) {
+                if (!valid(x)) continue;
+                acc = __dadd_rn(acc, row_elem(krow(x), i, s.dtype));
+                ++cnt;
+            }
+            mean[i] = static_cast<float>(acc / static_cast<double>(cnt));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double acc = 0.0;
+            for (int i = 0; i < s.w; ++i) acc = fma(static_cast<double>(mean[i]), static_cast<double>(mean[i]), acc);
+            sh_mnorm = sqrt(acc);
+        }
+        __syncthreads();
+    }
+    const double mnorm = sh_mnorm;
+    double bv = -INFINITY;
+    int bx = 0x7FFFFFFF;
+    for (int x = threadIdx.x; x < X; x += blockDim.x) {
+        if (!valid(x)) continue;
+        const long long p = pos_of(x);
+        double v;
+        if (rule == PE_TOKEN_AT_POSITION) {
+            if (p != arg) continue;
+            v = 0.0;
+        } else if (rule == PE_TOKEN_STREAMING) {
+            if (p < arg) continue;
+            v = 0.0;
+        } else {
+            if (p == newest) continue;
+            const uint8_t* kr = krow(x);
+            const double kn = sqrt(row_sumsq_f(kr, s.w, s.dtype));
+            if (rule == PE_TOKEN_MAX_KEY_NORM) {
+                v = kn;
+            } else {  // cosine_similarity (policy.cpp:103-115)
+                if (kn < kNormEps || mnorm < kNormEps) {
+                    v = -1.0;
+                } else {
+                    double dot = 0.0;
+                    for (int i = 0; i < s.w; ++i) dot = fma(row_elem(kr, i, s.dtype), static_cast<double>(mean[i]), dot);
+                    v = __ddiv_rn(dot, __dmul_rn(kn, mnorm));
+                }
+            }
+        }
+        if (v > bv) {  // x ascending per thread: ties keep the first
+            bv = v;
+            bx = x;
+        }
+    }
+    sh_val[threadIdx.x] = bv;
+    sh_x[threadIdx.x] = bx;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int i = 1; i < (int)blockDim.x; ++i) {
+        if (sh_x[i] == 0x7FFFFFFF) continue;
+        if (bx == 0x7FFFFFFF || sh_val[i] > bv || (sh_val[i] == bv && sh_x[i] < bx)) {
+            bv = sh_val[i];
+            bx = sh_x[i];
+        }
+    }
+    if (bx == 0x7FFFFFFF) {
+        if (rule == PE_TOKEN_AT_POSITION) set_status(s.status, PE_UNKNOWN_POSITION);
+        *out = -1;
+        return;
+    }
+    const int j = bx / s.B, sl = bx % s.B;
+    const int page = row[j];
+    *out = pos_of(bx);
+    s.holes[page] |= 1ull << sl;
+    s.retained[t] -= 1;
+    const int cursor = (j == N - 1) ? nf : s.B;
+    const int fill = page_fill(s, page, cursor);
+    if (fill == 0) {  // drained: release whole and close ranks
+        s.holes[page] = 0ull;
+        const int top = *s.top;
+        s.stack[top] = page;
+        *s.top = top + 1;
+        for (int k = j; k < N - 1; ++k) row[k] = row[k + 1];
+        row[N - 1] = -1;
+        s.num_pages[t] = N - 1;
+        if (j == N - 1) s.newest_fill[t] = (N - 1 > 0) ? s.B : 0;
+    } else if (cursor == s.B) {  // keep the cached page mean of a full page current
+        double sum = 0.0;
+        for (int k = 0; k < s.B; ++k)
+            if (!slot_hole(s, page, k)) sum += s.token_scores[(int64_t)page * s.B + k];
+        s.page_scores[page] = sum / static_cast<double>(fill);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Prefill scoring + selection for the InvKeyL2 / KeyDiff baselines
+// (compress_by_score, policy.cpp:90-101, with the scores of policy.cpp:212-216
+// and :244-260): one thread per token scores it, a bitonic sort orders
+// (score, position) ascending (rank_tokens, importance.cpp:41-60) and the
+// first k are flagged.
+__global__ void prompt_mean_key_kernel(const float* k, int n, int w, float* mean, double* mnorm) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < w; i += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int x = 0; x < n; ++x) acc = __dadd_rn(acc, static_cast<double>(k[(int64_t)x * w + i]));
+        mean[i] = static_cast<float>(acc / static_cast<double>(n));
+    }
+    __threadfence();
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0 && gridDim.x == 1) {
+        double acc = 0.0;
+        for (int i = 0; i < w; ++i) acc = fma(static_cast<double>(mean[i]), static_cast<double>(mean[i]), acc);
+        *mnorm = sqrt(acc);
+    }
+}
+
+__global__ void prompt_score_kernel(const float* k, int n, int w, int rule, const float* mean, const double* mnorm,
+                                    const long long* pos, int n_pad, double* score, long long* spos, int* sidx) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n_pad) return;
+    if (x >= n) {
+        score[x] = INFINITY;
+        spos[x] = 0x7FFFFFFFFFFFFFFFll;
+        sidx[x] = x;
+        return;
+    }
+    const float* kr = k + (int64_t)x * w;
+    double acc = 0.0;
+    for (int i = 0; i < w; ++i) acc = fma(static_cast<double>(kr[i]), static_cast<double>(kr[i]), acc);
+    const double kn = sqrt(acc);
+    double v;
+    if (rule == PE_TOKEN_MAX_KEY_NORM) {
+        v = 1.0 / fmax(kn, kNormEps);
+    } else {
+        const double mn = *mnorm;
+        double c;
+        if (kn < kNormEps || mn < kNormEps) {
+            c = -1.0;
+        } else {
+            double dot = 0.0;
+            for (int i = 0; i < w; ++i) dot = fma(static_cast<double>(kr[i]), static_cast<double>(mean[i]), dot);
+            c = __ddiv_rn(dot, __dmul_rn(kn, mn));
+        }
+        v = -c;
+    }
+    score[x] = v;
+    spos[x] = pos[x];
+    sidx[x] = x;
+}
+
+__global__ void bitonic_step_kernel(double* score, long long* spos, int* sidx, int n_pad, int j, int k) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_pad) return;
+    const int o = i ^ j;
+    if (o <= i) return;
+    const bool less_io = score[o] < score[i] || (score[o] == score[i] && spos[o] < spos[i]);
+    const bool up = (i & k) == 0;
+    if (less_io == up) {  // out of order for this direction: swap
+        const double a = score[i];
+        score[i] = score[o];
+        score[o] = a;
+        const long long b = spos[i];
+        spos[i] = spos[o];
+        spos[o] = b;
+        const int c = sidx[i];
+        sidx[i] = sidx[o];
+        sidx[o] = c;
+    }
+}
+
+__global__ void flag_first_kernel(const int* sidx, int k, uint8_t* flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k) flags[sidx[i]] = 1;
 }
 
 }  // namespace pe

@@ -26,10 +26,10 @@ REF = Path("/root/reference/proj")
 REF_TESTS = ["test_paged_store.cpp", "test_importance.cpp", "test_policies.cpp", "test_attention.cpp"]
 
 
-def _cxx(srcs: list[Path], out: Path, extra_inc: list[Path]) -> Path:
+def _cxx(srcs: list[Path], out: Path, extra_inc: list[Path], shim_main: bool = True) -> Path:
     OUT.mkdir(parents=True, exist_ok=True)
     cmd = ["g++", "-std=c++20", "-O2", "-g", f"-I{HERE}", f"-I{ROOT / 'include'}",
-           *[f"-I{p}" for p in extra_inc], *map(str, srcs), str(HERE / "shim_main.cpp"),
+           *[f"-I{p}" for p in extra_inc], *map(str, srcs), *([str(HERE / "shim_main.cpp")] if shim_main else []),
            f"-L{LIB_DIR}", "-lpagedevict_b200", "-lpe_b200", f"-Wl,-rpath,{LIB_DIR}",
            "-Wl,-rpath,$ORIGIN/../../../paper_2509_04377_b200/lib", "-lpthread", "-o", str(out)]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -55,12 +55,34 @@ def build_facade_tests() -> Path:
     return _cxx([HERE / "test_facade.cpp", obj], OUT / "facade_tests", [])
 
 
+REF_CORE = ["page_pool.cpp", "block_table.cpp", "importance.cpp", "policy.cpp", "attention.cpp"]
+
+
+def build_scenario() -> tuple[Path, Path | None]:
+    """scenario_trace.cpp twice: against the façade (tests/cpp/_build/scenario_b200)
+    and, where /root/reference exists, against the UNMODIFIED reference sources
+    (oracle/_ref/scenario_ref — reference build outputs live under oracle/_ref)."""
+    b200 = _cxx([HERE / "scenario_trace.cpp"], OUT / "scenario_b200", [], shim_main=False)
+    ref_out = None
+    if REF.exists():
+        ref_dir = ROOT / "oracle" / "_ref"
+        ref_dir.mkdir(parents=True, exist_ok=True)
+        ref_out = ref_dir / "scenario_ref"
+        cmd = ["g++", "-std=c++20", "-O2", f"-I{REF / 'core' / 'include'}", str(HERE / "scenario_trace.cpp"),
+               *[str(REF / "core" / "src" / f) for f in REF_CORE], "-lpthread", "-o", str(ref_out)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"g++ failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stderr[-8000:]}")
+    return b200, ref_out
+
+
 def build_all() -> None:
     from paper_2509_04377_b200 import _build
 
     _build.build()
     build_facade_tests()
     build_reference_conformance()
+    build_scenario()
 
 
 if __name__ == "__main__":
