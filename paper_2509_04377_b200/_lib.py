@@ -79,9 +79,14 @@ def load() -> C.CDLL:
     global _lib
     with _lock:
         if _lib is None:
-            path = _build.build()
+            import os
+
+            # PE_LIB: an alternative build of the same library (A/B timing runs)
+            path = os.environ.get("PE_LIB") or _build.build()
             lib = C.CDLL(str(path))
             for name, (res, args) in SIGNATURES.items():
+                if not hasattr(lib, name) and os.environ.get("PE_LIB"):
+                    continue  # older A/B build without the newest entry points
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -268,7 +268,7 @@ __device__ __forceinline__ void push_victims_if_last(const DevState& s, int n, i
 // slot-order sum / fill (score_pages -> page_score, importance.cpp:19-39).
 // The last CTA of the table (atomic ticket) takes the argmin and evicts; the
 // last CTA of the grid pushes the released pages.
-template <int SV>
+template <int SV, bool HOLES>
 __global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
     DevState s, TableSet ts, int pages_per_cta, double* scratch, int32_t* tickets, int32_t* vpage,
     int32_t* victims, unsigned long long grid_last) {
@@ -307,19 +307,19 @@ __global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
                 const uint8_t* base = s.pages + (int64_t)id * page_bytes;
                 const double S = pair_token_score<SV>(base + ko, base + vo, true, s.w, s.dtype);
                 double sum = 0.0;
-                if (!s.holes_on) {
+                if constexpr (!HOLES) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
                     if (lane == 0) page_mean[lp] = sum / 16.0;
                 } else {  // mean over the occupied slots (page_score, importance.cpp:19-30)
                     const unsigned long long hm = s.holes[id];
                     int cnt = 0;
+#pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         const double x = __shfl_sync(0xFFFFFFFFu, S, 2 * j);
-                        if (!((hm >> j) & 1ull)) {
-                            sum += x;
-                            ++cnt;
-                        }
+                        const bool occ = !((hm >> j) & 1ull);
+                        sum += occ ? x : 0.0;  // S >= +0: adding +0 leaves the sum unchanged
+                        cnt += occ;
                     }
                     if (lane == 0) page_mean[lp] = sum / static_cast<double>(cnt);
                 }
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
                     const int ns = min(16, s.B - s0);
                     for (int j = 0; j < ns; ++j) {
                         const double x = __shfl_sync(0xFFFFFFFFu, S, 2 * j);
-                        if (!slot_hole(s, id, s0 + j)) {
+                        if (!(HOLES && slot_hole(s, id, s0 + j))) {
                             sum += x;
                             ++cnt;
                         }
@@ -370,7 +370,11 @@ template <int SV>
 void launch_evict_score(dim3 grid, int threads, cudaStream_t st, const DevState& s, const TableSet& ts, int ppc,
                         double* scratch, int32_t* tickets, int32_t* vpage, int32_t* victims,
                         unsigned long long grid_last) {
-    evict_score_kernel<SV><<<grid, threads, 0, st>>>(s, ts, ppc, scratch, tickets, vpage, victims, grid_last);
+    // hole-aware variant only after the table API made holes (no runtime check in the hot loop)
+    if (s.holes_on)
+        evict_score_kernel<SV, true><<<grid, threads, 0, st>>>(s, ts, ppc, scratch, tickets, vpage, victims, grid_last);
+    else
+        evict_score_kernel<SV, false><<<grid, threads, 0, st>>>(s, ts, ppc, scratch, tickets, vpage, victims, grid_last);
 }
 
 template <int SV>
