@@ -17,7 +17,7 @@
 // snapshots of a device page, refreshed on each call; mutating a snapshot
 // (Page::write / evict / reset) does not write back.
 //
-// Differences from the reference (DESIGN.md §10):
+// Differences from the reference (DESIGN.md §9):
 //  * a pool's row width is fixed by the first token appended (or
 //    PoolOptions::row_width): narrower tokens are zero-padded (norms,
 //    scores and dot products are unchanged), wider ones throw LengthMismatch;
