@@ -33,6 +33,39 @@ __device__ __forceinline__ float elem_f32(const uint8_t* row, int idx, int dtype
     return reinterpret_cast<const float*>(row)[idx];
 }
 
+// Split-K completion: every split CTA of table i writes its partial, then
+// takes a ticket; the CTA holding the last ticket merges all splits
+// (out = sum_s o_s 2^(m_s - M) / sum_s l_s 2^(m_s - M)) and rearms the
+// ticket. Replaces a separate merge launch.
+__device__ __forceinline__ void merge_if_last(const DevState& s, const AttnArgs& a, int i, int d) {
+    __shared__ int is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(a.tickets + i, 1) == a.splits - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const int H = s.tab_heads;
+    const int h = i % H;
+    const int seq = i / H;
+    const int G = a.G;
+    for (int x = threadIdx.x; x < G * d; x += blockDim.x) {
+        const int g = x / d;
+        float mm = -INFINITY;
+        for (int sp = 0; sp < a.splits; ++sp) mm = fmaxf(mm, __ldcg(a.part_ml + (((int64_t)i * a.splits + sp) * G + g) * 2));
+        float ll = 0.f, oo = 0.f;
+        for (int sp = 0; sp < a.splits; ++sp) {
+            const int64_t pidx = ((int64_t)i * a.splits + sp) * G + g;
+            const float ms = __ldcg(a.part_ml + pidx * 2);
+            const float c = (ms == -INFINITY) ? 0.f : exp2f(ms - mm);
+            ll += __ldcg(a.part_ml + pidx * 2 + 1) * c;
+            oo += __ldcg(a.part_o + pidx * d + (x % d)) * c;
+        }
+        a.out[((int64_t)seq * a.n_q_heads + h * G + g) * d + (x % d)] = oo / ll;
+    }
+    if (threadIdx.x == 0) a.tickets[i] = 0;
+}
+
 __global__ void __launch_bounds__(kAttnThreads) attention_split_kernel(DevState s, AttnArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
@@ -244,6 +277,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_split_kernel(DevState 
             a.part_ml[pidx * 2 + 1] = ll;
         }
     }
+    merge_if_last(s, a, i, d);
 }
 
 // ---------------------------------------------------------------------------
@@ -459,6 +493,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_mma_kernel(DevState
             a.part_ml[pidx * 2 + 1] = ll;
         }
     }
+    merge_if_last(s, a, i, D);
 }
 
 size_t attention_mma_smem(int d, int G) {
@@ -474,30 +509,6 @@ void launch_attention_mma(int d, dim3 grid, size_t smem, cudaStream_t st, const 
 const void* attention_mma_fn(int d) {
     return d == 128 ? reinterpret_cast<const void*>(attention_mma_kernel<128>)
                     : reinterpret_cast<const void*>(attention_mma_kernel<64>);
-}
-
-// merge the split partials: out = sum_s o_s * 2^(m_s - M) / sum_s l_s * 2^(m_s - M)
-__global__ void __launch_bounds__(128) attention_merge_kernel(DevState s, AttnArgs a) {
-    const int i = blockIdx.x;  // launch table
-    const int H = s.tab_heads;
-    const int h = i % H;
-    const int seq = i / H;
-    const int G = a.G;
-    const int d = s.w;
-    for (int x = threadIdx.x; x < G * d; x += blockDim.x) {
-        const int g = x / d;
-        float mm = -INFINITY;
-        for (int sp = 0; sp < a.splits; ++sp) mm = fmaxf(mm, a.part_ml[(((int64_t)i * a.splits + sp) * G + g) * 2]);
-        float ll = 0.f, oo = 0.f;
-        for (int sp = 0; sp < a.splits; ++sp) {
-            const int64_t pidx = ((int64_t)i * a.splits + sp) * G + g;
-            const float ms = a.part_ml[pidx * 2];
-            const float c = (ms == -INFINITY) ? 0.f : exp2f(ms - mm);
-            ll += a.part_ml[pidx * 2 + 1] * c;
-            oo += a.part_o[pidx * d + (x % d)] * c;
-        }
-        a.out[((int64_t)seq * a.n_q_heads + h * G + g) * d + (x % d)] = oo / ll;
-    }
 }
 
 }  // namespace pe

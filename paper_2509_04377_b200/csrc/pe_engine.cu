@@ -82,14 +82,17 @@ struct pe_engine {
     int32_t* h_tab_pagebase = nullptr;  // pinned
     // staging ring for host buffers: H2D copies run on copy_stream, overlapping
     // the engine's kernels; slot reuse is guarded by "consumed" events
-    static constexpr int kRing = 8;
+    static constexpr int kRing = 64;  // a whole decode cycle of host inputs can be staged ahead
+    static constexpr size_t kRingSlotCap = size_t(64) << 20;  // larger inputs get private buffers
     struct Slot {
-        uint8_t* buf = nullptr;
-        size_t bytes = 0;
+        uint8_t* big = nullptr;          // private buffer for inputs > kRingSlotCap
+        size_t big_bytes = 0;
         cudaEvent_t ready = nullptr;     // copy done (copy_stream)
         cudaEvent_t consumed = nullptr;  // last reader done (compute stream)
     } ring[kRing];
     int ring_next = 0;
+    uint8_t* ring_arena = nullptr;       // kRing slots of ring_slot_bytes each
+    size_t ring_slot_bytes = 0;
     int pending[4];                      // slots staged by the current call
     int n_pending = 0;
     cudaStream_t copy_stream = nullptr;
@@ -107,6 +110,7 @@ struct pe_engine {
     // table-granular API (pe_table_*, pe_pool_*)
     int32_t* alloc_out = nullptr;
     int64_t* tok_out = nullptr;
+    int32_t* attn_tickets = nullptr;  // [n_tables] split-K completion tickets
     double* attend_logits = nullptr;
     size_t attend_logits_elems = 0;
     float* attend_out = nullptr;
@@ -142,20 +146,35 @@ pe_status as_device(pe_engine* e, const void* p, size_t bytes, cudaStream_t st, 
     const int k = e->ring_next;
     e->ring_next = (e->ring_next + 1) % pe_engine::kRing;
     pe_engine::Slot& sl = e->ring[k];
-    if (sl.bytes < bytes) {
-        PE_CUDA(cudaEventSynchronize(sl.consumed));
-        if (sl.buf) PE_CUDA(cudaFree(sl.buf));
-        sl.buf = nullptr;
-        sl.bytes = 0;
-        PE_CUDA(cudaMalloc(&sl.buf, bytes));
-        sl.bytes = bytes;
+    if (bytes > pe_engine::kRingSlotCap) {
+        // large inputs (a prefill layer from host memory): a private buffer per slot
+        if (sl.big_bytes < bytes) {
+            PE_CUDA(cudaEventSynchronize(sl.consumed));
+            if (sl.big) PE_CUDA(cudaFree(sl.big));
+            sl.big = nullptr;
+            sl.big_bytes = 0;
+            PE_CUDA(cudaMalloc(&sl.big, bytes));
+            sl.big_bytes = bytes;
+        }
+    } else if (e->ring_slot_bytes < bytes) {
+        // grow the whole ring at once (one arena, every slot the same size)
+        // so no slot has to grow later in the middle of a pipelined cycle
+        for (auto& other : e->ring) PE_CUDA(cudaEventSynchronize(other.consumed));
+        PE_CUDA(cudaStreamSynchronize(e->copy_stream));
+        const size_t slot = (bytes + 255) & ~size_t(255);
+        if (e->ring_arena) PE_CUDA(cudaFree(e->ring_arena));
+        e->ring_arena = nullptr;
+        e->ring_slot_bytes = 0;
+        PE_CUDA(cudaMalloc(&e->ring_arena, slot * pe_engine::kRing));
+        e->ring_slot_bytes = slot;
     }
+    uint8_t* dst = bytes > pe_engine::kRingSlotCap ? sl.big : e->ring_arena + (size_t)k * e->ring_slot_bytes;
     PE_CUDA(cudaStreamWaitEvent(e->copy_stream, sl.consumed, 0));
-    PE_CUDA(cudaMemcpyAsync(sl.buf, p, bytes, cudaMemcpyHostToDevice, e->copy_stream));
+    PE_CUDA(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, e->copy_stream));
     PE_CUDA(cudaEventRecord(sl.ready, e->copy_stream));
     PE_CUDA(cudaStreamWaitEvent(st, sl.ready, 0));
     if (e->n_pending < 4) e->pending[e->n_pending++] = k;
-    *out = sl.buf;
+    *out = dst;
     return PE_OK;
 }
 
@@ -291,6 +310,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         dalloc(&s.holes, (size_t)cap) != cudaSuccess ||
         dalloc(&e->vpage, n_tables) != cudaSuccess || dalloc(&e->ctl, 1) != cudaSuccess ||
         dalloc(&e->alloc_out, 1) != cudaSuccess || dalloc(&e->tok_out, 1) != cudaSuccess ||
+        dalloc(&e->attn_tickets, n_tables) != cudaSuccess ||
         dalloc(&e->lb_status, (size_t)n_tables / 64 + 2) != cudaSuccess ||
         dalloc(&e->rank, n_tables) != cudaSuccess || dalloc(&e->work, n_tables) != cudaSuccess ||
         dalloc(&e->victims, n_tables) != cudaSuccess || dalloc(&e->tickets, n_tables) != cudaSuccess ||
@@ -326,6 +346,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             cudaMemset(s.evict_count, 0, sizeof(unsigned long long)) != cudaSuccess ||
             cudaMemset(s.grid_ctr, 0, sizeof(unsigned long long)) != cudaSuccess ||
             cudaMemset(e->tickets, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
+            cudaMemset(e->attn_tickets, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
             cudaMemset(e->lb_status, 0, sizeof(unsigned long long) * ((size_t)n_tables / 64 + 2)) != cudaSuccess ||
             cudaMemset(e->ctl, 0, sizeof(LaunchCtl)) != cudaSuccess ||
             cudaMemset(s.positions, 0xFF, sizeof(int32_t) * (size_t)cap * s.B) != cudaSuccess ||
@@ -385,12 +406,13 @@ pe_status pe_engine_destroy(pe_engine* e) {
                    e->work, e->victims, e->tickets, e->evict_scratch, e->tab_len, e->tab_tok0,
                    e->tab_pagebase, e->evicted_dev, e->part_o,
                    e->part_ml, e->out_stage, e->tab_keybase, e->keys, e->surv, e->lb_status,
-                   e->alloc_out, e->tok_out, e->attend_logits, e->attend_out, e->attend_ws};
+                   e->alloc_out, e->tok_out, e->attn_tickets, e->attend_logits, e->attend_out, e->attend_ws};
     for (void* p : dev) {
         if (p) cudaFree(p);
     }
+    if (e->ring_arena) cudaFree(e->ring_arena);
     for (auto& sl : e->ring) {
-        if (sl.buf) cudaFree(sl.buf);
+        if (sl.big) cudaFree(sl.big);
         if (sl.ready) cudaEventDestroy(sl.ready);
         if (sl.consumed) cudaEventDestroy(sl.consumed);
     }
@@ -690,6 +712,7 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
     a.out = out_dev ? out : e->out_stage;
     a.part_o = e->part_o;
     a.part_ml = e->part_ml;
+    a.tickets = e->attn_tickets;
     a.layer = layer;
     a.G = G;
     a.n_q_heads = n_q_heads;
@@ -708,11 +731,10 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
         if (smem > (size_t)e->max_dyn_attn) return fail(PE_INVALID_ARG, "attention tile exceeds shared memory");
         attention_split_kernel<<<dim3(splits, n_tab), 128, smem, st>>>(s, a);
     }
-    attention_merge_kernel<<<n_tab, 128, 0, st>>>(s, a);
     mark_consumed(e, st);
     r = check_launch(e, "attention");
     if (r != PE_OK) return r;
-    e->stats.kernel_launches += 2;
+    e->stats.kernel_launches += 1;
     e->stats.attention_calls += 1;
     if (!out_dev) {
         PE_CUDA(cudaMemcpyAsync(out, e->out_stage, sizeof(float) * out_elems, cudaMemcpyDeviceToHost, st));

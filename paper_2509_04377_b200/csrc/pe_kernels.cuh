@@ -55,6 +55,7 @@ struct AttnArgs {
     float* out;              // [n_seqs][n_q_heads][d]
     float* part_o;           // [n_tab][splits][G][d] split partial outputs
     float* part_ml;          // [n_tab][splits][G][2]  (max, sum)
+    int32_t* tickets;        // [n_tab] split completion tickets (zero between launches)
     int32_t layer, G, n_q_heads, splits, pages_per_split;
     float scale_log2;        // log2(e)/sqrt(d)
 };
@@ -63,7 +64,6 @@ __global__ void attention_split_kernel(DevState s, AttnArgs a);
 size_t attention_mma_smem(int d, int G);
 void launch_attention_mma(int d, dim3 grid, size_t smem, cudaStream_t st, const DevState& s, const AttnArgs& a);
 const void* attention_mma_fn(int d);
-__global__ void attention_merge_kernel(DevState s, AttnArgs a);
 
 // table-granular kernels (pe_table.cu)
 __global__ void pool_allocate_kernel(DevState s, int32_t* out);
