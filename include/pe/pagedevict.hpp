@@ -371,3 +371,7 @@ AttentionDetail attend_detailed(const AttentionInputs& inputs);
 double output_deviation(std::span<const float> a, std::span<const float> b);
 
 }  // namespace pagedevict
+
+// Integration self-test (one PagedEviction table on the device, invariants
+// checked); returns 0 and a summary in msg, or 1 and the error.
+extern "C" int pagedevict_facade_selftest(char* msg, int cap);

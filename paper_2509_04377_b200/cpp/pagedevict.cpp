@@ -13,6 +13,7 @@
 #include "pe/pagedevict.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -925,3 +926,60 @@ double output_deviation(std::span<const float> a, std::span<const float> b) {
 }
 
 }  // namespace pagedevict
+
+// Integration self-test for smoke checks (`__graft_entry__.smoke()` calls it
+// through ctypes): one PagedEviction table through prefill_compress, 64
+// decode steps and attend on the device, checked against the reference's
+// invariants (policy.cpp:143-155: floor(D/B) page evictions, retained
+// within (C-B, C+B], pool conservation; softmax weights sum to one).
+extern "C" int pagedevict_facade_selftest(char* msg, int cap) {
+    using namespace pagedevict;
+    auto say = [&](const std::string& m) {
+        if (msg != nullptr && cap > 0) std::snprintf(msg, static_cast<std::size_t>(cap), "%s", m.c_str());
+    };
+    try {
+        const std::uint32_t B = 16;
+        const std::size_t C = 64, w = 32, L = 200, D = 64;
+        PagePool pool(C / B + 2, B);
+        BlockTable table(pool);
+        PolicyConfig cfg;
+        cfg.cache_budget = C;
+        cfg.page_size = B;
+        auto policy = make_policy(cfg);
+        std::uint64_t x = 0x9E3779B97F4A7C15ull;
+        auto nrm = [&]() {  // deterministic pseudo-normal values
+            x ^= x << 13, x ^= x >> 7, x ^= x << 17;
+            return static_cast<float>(static_cast<double>(x >> 11) / 9007199254740992.0 * 2.0 - 1.0);
+        };
+        auto tok = [&](std::uint64_t p) {
+            std::vector<float> k(w), v(w);
+            for (auto& a : k) a = nrm();
+            for (auto& a : v) a = nrm();
+            return make_kv(std::move(k), std::move(v), p);
+        };
+        std::vector<KvVector> prompt;
+        for (std::uint64_t i = 0; i < L; ++i) prompt.push_back(tok(i));
+        auto pre = policy->prefill_compress(std::move(prompt));
+        if (pre.retained.size() != C || pre.decision.positions.size() != L - C) throw Error("prefill size");
+        for (auto& kv : pre.retained) table.append_token(std::move(kv));
+        std::size_t evictions = 0;
+        for (std::uint64_t s = 1; s <= D; ++s) {
+            const auto d = policy->decode_step(table, tok(L + s - 1), static_cast<std::int64_t>(s));
+            evictions += d.kind == EvictionDecision::Kind::Page;
+            if (table.retained_len() > C + B || table.retained_len() <= C - B) throw Error("retained bound");
+        }
+        if (evictions != D / B) throw Error("expected " + std::to_string(D / B) + " page evictions");
+        if (pool.allocated() + pool.free_count() != pool.capacity()) throw Error("pool conservation");
+        std::vector<float> q(w);
+        for (auto& a : q) a = nrm();
+        const auto det = attend_detailed(AttentionInputs{q, &table, 2, static_cast<std::uint32_t>(w / 2)});
+        for (const double s : det.weight_sums)
+            if (std::fabs(s - 1.0) > 1e-12) throw Error("softmax weights");
+        say("facade ok: " + std::to_string(evictions) + " page evictions, retained " +
+            std::to_string(table.retained_len()));
+        return 0;
+    } catch (const std::exception& e) {
+        say(e.what());
+        return 1;
+    }
+}
