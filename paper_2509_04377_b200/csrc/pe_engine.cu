@@ -694,6 +694,7 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
     pe_status r = as_device(e, q, (size_t)s.n_seqs * n_q_heads * s.row_bytes, st, &dq);
     if (r != PE_OK) return r;
     int splits = std::max(1, (e->sm_count * 8 + n_tab - 1) / n_tab);
+    if (const char* sv = std::getenv("PE_ATTN_SPLITS")) splits = std::max(1, std::atoi(sv));
     splits = std::min(splits, std::max(1, (s.max_pages + 3) / 4));
     const int pps = (s.max_pages + splits - 1) / splits;
     splits = (s.max_pages + pps - 1) / pps;
