@@ -111,6 +111,15 @@ struct pe_engine {
     int32_t* alloc_out = nullptr;
     int64_t* tok_out = nullptr;
     int32_t* attn_tickets = nullptr;  // [n_tables] split-K completion tickets
+    // fused prefill schedule (prefill_fused_kernel)
+    int32_t* h_items = nullptr;          // pinned
+    size_t h_items_elems = 0;
+    int32_t* items = nullptr;
+    size_t items_elems = 0;
+    int32_t* h_seq_units = nullptr;      // pinned [n_seqs]
+    int32_t* seq_units = nullptr;        // [n_seqs]
+    int32_t* seq_done = nullptr;         // [n_seqs]
+    int32_t* work_ctr = nullptr;
     double* attend_logits = nullptr;
     size_t attend_logits_elems = 0;
     float* attend_out = nullptr;
@@ -311,6 +320,8 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         dalloc(&e->vpage, n_tables) != cudaSuccess || dalloc(&e->ctl, 1) != cudaSuccess ||
         dalloc(&e->alloc_out, 1) != cudaSuccess || dalloc(&e->tok_out, 1) != cudaSuccess ||
         dalloc(&e->attn_tickets, n_tables) != cudaSuccess ||
+        dalloc(&e->seq_units, c.n_seqs) != cudaSuccess || dalloc(&e->seq_done, c.n_seqs) != cudaSuccess ||
+        dalloc(&e->work_ctr, 1) != cudaSuccess ||
         dalloc(&e->lb_status, (size_t)n_tables / 64 + 2) != cudaSuccess ||
         dalloc(&e->rank, n_tables) != cudaSuccess || dalloc(&e->work, n_tables) != cudaSuccess ||
         dalloc(&e->victims, n_tables) != cudaSuccess || dalloc(&e->tickets, n_tables) != cudaSuccess ||
@@ -327,7 +338,8 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
     if (cudaMallocHost(&e->h_tab_len, sizeof(int32_t) * c.n_seqs * tab_heads) != cudaSuccess ||
         cudaMallocHost(&e->h_tab_tok0, sizeof(int64_t) * c.n_seqs * tab_heads) != cudaSuccess ||
         cudaMallocHost(&e->h_tab_pagebase, sizeof(int32_t) * c.n_seqs * tab_heads) != cudaSuccess ||
-        cudaMallocHost(&e->h_tab_keybase, sizeof(int64_t) * c.n_seqs * tab_heads) != cudaSuccess) {
+        cudaMallocHost(&e->h_tab_keybase, sizeof(int64_t) * c.n_seqs * tab_heads) != cudaSuccess ||
+        cudaMallocHost(&e->h_seq_units, sizeof(int32_t) * c.n_seqs) != cudaSuccess) {
         cudaGetLastError();
         return cleanup_fail(fail(PE_CUDA_ERROR, "pinned allocation failed"));
     }
@@ -386,7 +398,8 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         if (!allow(reinterpret_cast<const void*>(prefill_select_kernel), &e->max_dyn_prefill) ||
             !allow(reinterpret_cast<const void*>(attention_split_kernel), &e->max_dyn_attn) ||
             !allow(attention_mma_fn(64), &mma64) || !allow(attention_mma_fn(128), &mma128) ||
-            !allow(reinterpret_cast<const void*>(prefill_select_cta_kernel), &sel_cta)) {
+            !allow(reinterpret_cast<const void*>(prefill_select_cta_kernel), &sel_cta) ||
+            !allow(prefill_fused_fn(e->variant), &sel_cta)) {
             cudaGetLastError();
             return cleanup_fail(fail(PE_CUDA_ERROR, "cudaFuncSetAttribute(max dynamic smem) failed"));
         }
@@ -406,7 +419,7 @@ pe_status pe_engine_destroy(pe_engine* e) {
                    e->work, e->victims, e->tickets, e->evict_scratch, e->tab_len, e->tab_tok0,
                    e->tab_pagebase, e->evicted_dev, e->part_o,
                    e->part_ml, e->out_stage, e->tab_keybase, e->keys, e->surv, e->lb_status,
-                   e->alloc_out, e->tok_out, e->attn_tickets, e->attend_logits, e->attend_out, e->attend_ws};
+                   e->alloc_out, e->tok_out, e->attn_tickets, e->items, e->seq_units, e->seq_done, e->work_ctr, e->attend_logits, e->attend_out, e->attend_ws};
     for (void* p : dev) {
         if (p) cudaFree(p);
     }
@@ -425,6 +438,8 @@ pe_status pe_engine_destroy(pe_engine* e) {
     if (e->h_tab_tok0) cudaFreeHost(e->h_tab_tok0);
     if (e->h_tab_pagebase) cudaFreeHost(e->h_tab_pagebase);
     if (e->h_tab_keybase) cudaFreeHost(e->h_tab_keybase);
+    if (e->h_items) cudaFreeHost(e->h_items);
+    if (e->h_seq_units) cudaFreeHost(e->h_seq_units);
     cudaGetLastError();
     delete e;
     return PE_OK;
@@ -514,6 +529,68 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     a.chunk_cap = use_cta_select ? max_len : chunk_cap;  // keys held in smem per CTA
     if (total_pages > INT32_MAX) return fail(PE_POOL_EXHAUSTED, "page pool exhausted");
     plan_prefill_kernel<<<1, 1024, 0, st>>>(s, a, static_cast<int32_t>(total_pages), e->ctl);
+    // Opt-in (PE_PREFILL_FUSED=1): the persistent single-launch variant. On
+    // cfg3 it measures 2.23-2.40 ms/layer against 1.99-2.01 ms for the
+    // multi-kernel wave pipeline below (its 1024-thread CTAs keep fewer
+    // loads in flight while scoring), so the wave pipeline is the default.
+    const char* fz = std::getenv("PE_PREFILL_FUSED");
+    if (use_cta_select && fz != nullptr && std::strcmp(fz, "1") == 0) {
+        // one persistent launch: score units and per-table select+copy items,
+        // X(q) scheduled after S(q+1) (prefill_fused_kernel)
+        int kUnitTokens = 1024;
+        if (const char* ut = std::getenv("PE_UNIT_TOKENS")) kUnitTokens = std::max(16, std::atoi(ut));
+        int64_t n_items = 0;
+        for (int q = 0; q < n_seqs; ++q)
+            n_items += (cu_seqlens[q + 1] - cu_seqlens[q] + kUnitTokens - 1) / kUnitTokens + H;
+        if (n_items >= INT32_MAX || n_seqs > 32767) return fail(PE_INVALID_ARG, "prefill schedule too large");
+        if ((size_t)n_items > e->h_items_elems) {
+            if (e->h_items) PE_CUDA(cudaFreeHost(e->h_items));
+            e->h_items = nullptr;
+            e->h_items_elems = 0;
+            PE_CUDA(cudaMallocHost(&e->h_items, sizeof(int32_t) * n_items));
+            e->h_items_elems = (size_t)n_items;
+        }
+        if ((r = ensure_t(&e->items, &e->items_elems, (size_t)n_items)) != PE_OK) return r;
+        // lag: X(q) follows S(q + lag), with enough score units in between
+        // (~2 per CTA) that the sequence's scoring has finished when its
+        // select items are claimed (no CTA spins while others still score it)
+        const int64_t units_total = n_items - (int64_t)n_seqs * H;
+        const int64_t per_seq = std::max<int64_t>(1, units_total / n_seqs);
+        int lag = (int)std::min<int64_t>(n_seqs, (2 * e->sm_count + per_seq - 1) / per_seq);
+        if (const char* lg = std::getenv("PE_FUSED_LAG")) lag = std::max(1, std::atoi(lg));
+        int64_t k = 0;
+        for (int q = 0; q < n_seqs + lag; ++q) {
+            if (q < n_seqs) {
+                const int u = (cu_seqlens[q + 1] - cu_seqlens[q] + kUnitTokens - 1) / kUnitTokens;
+                e->h_seq_units[q] = u;
+                if (u > 0xFFFF) return fail(PE_INVALID_ARG, "prefill length exceeds the schedule encoding");
+                for (int j = 0; j < u; ++j) e->h_items[k++] = (q << 16) | j;
+            }
+            const int qx = q - lag;
+            if (qx >= 0 && qx < n_seqs)
+                for (int h = 0; h < H; ++h) e->h_items[k++] = static_cast<int32_t>(0x80000000u | (qx << 16) | h);
+        }
+        PE_CUDA(cudaMemcpyAsync(e->items, e->h_items, sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
+        PE_CUDA(cudaMemcpyAsync(e->seq_units, e->h_seq_units, sizeof(int32_t) * n_seqs, cudaMemcpyHostToDevice, st));
+        PE_CUDA(cudaEventRecord(e->ev_meta, st));
+        PE_CUDA(cudaMemsetAsync(e->seq_done, 0, sizeof(int32_t) * n_seqs, st));
+        PE_CUDA(cudaMemsetAsync(e->work_ctr, 0, sizeof(int32_t), st));
+        const size_t sel_smem =
+            (((size_t)max_len * 4 + 15) & ~size_t(15)) + kSelHistCopies * 2048 * 4 + kSelCandCap * 4;
+        const int grid = (int)std::min<int64_t>(e->sm_count, n_items);
+        launch_prefill_fused_any(e->variant, grid, sel_smem, st, s, a, e->ctl, e->items, (int)n_items, e->work_ctr,
+                                 e->seq_done, e->seq_units, kUnitTokens);
+        mark_consumed(e, st);
+        r = check_launch(e, "prefill_fused_kernel");
+        if (r != PE_OK) return r;
+        e->stats.kernel_launches += 2;
+        e->stats.prefill_calls += 1;
+        e->stats.tokens_scored += (int64_t)tokens * H;
+        if (evicted_counts && !ev_dev) {
+            PE_CUDA(cudaMemcpyAsync(evicted_counts, e->evicted_dev, sizeof(int32_t) * n_tab, cudaMemcpyDeviceToHost, st));
+        }
+        return PE_OK;
+    }
     // Sequence waves ping-pong between the caller's stream and the engine's
     // aux stream: while one wave is in its latency-bound select, the other
     // stream's HBM-bound score / copy kernels keep the memory system busy.

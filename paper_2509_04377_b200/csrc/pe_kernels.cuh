@@ -39,6 +39,11 @@ constexpr int kSelHistCopies = 8;        // private histogram copies in the CTA 
 constexpr int kSelCandCap = 4096;        // boundary-bin candidates compacted after the first radix pass
 constexpr int kSelectCtaMaxLen = 34816;  // CTA-per-table select: 4 B of smem per token + 64 KB histograms + 16 KB candidates
 __global__ void prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
+// persistent fused prefill (score units + per-table select/copy), pe_prefill.cu
+void launch_prefill_fused_any(int variant, int grid, size_t smem, cudaStream_t st, const DevState& s,
+                              const PrefillArgs& a, const LaunchCtl* ctl, const int32_t* items, int n_items,
+                              int* work_ctr, int* seq_done, const int32_t* seq_units, int unit_tokens);
+const void* prefill_fused_fn(int variant);
 
 // host-side launchers of the row-geometry-specialised kernels (pe_score.cuh variants)
 void launch_append_any(int variant, int blocks, cudaStream_t st, const DevState& s, const TableSet& ts,

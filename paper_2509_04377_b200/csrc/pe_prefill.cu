@@ -478,14 +478,14 @@ __device__ __forceinline__ int block_find_digit(const uint32_t* hist, int nbins,
     return bc[0];
 }
 
-__global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
-    extern __shared__ __align__(16) uint8_t smem[];
+// Select of launch table i by the whole CTA (1024 threads); `smem` is the
+// dynamic shared memory (hi words, histogram copies, candidates).
+__device__ __noinline__ void select_table_cta(const DevState& s, const PrefillArgs& a, int i, uint8_t* smem,
+                                              const LaunchCtl* ctl) {
     __shared__ uint32_t hist[2048];  // reduced histogram
     __shared__ int scan_sm[33];
     __shared__ int bc[4];
     __shared__ unsigned int mm[2];
-    if (ctl->abort) return;
-    const int i = blockIdx.x;
     const int tid = threadIdx.x;
     const int nthr = blockDim.x;
     const int L = a.tab_len[i];
@@ -759,18 +759,22 @@ __global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s,
     }
 }
 
+__global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    if (ctl->abort) return;
+    select_table_cta(s, a, blockIdx.x, smem, ctl);
+}
+
 // ---------------------------------------------------------------------------
 // prefill_copy_kernel: one warp per destination page. Lane pair r moves the
 // page's slot r: survivor q = page*B + r (position order) -> K and V rows
 // with 256-bit loads/stores, position and cached score beside the page; the
 // warp then sums the B scores in slot order (page_score, importance.cpp:19-30)
 // for a full page. Grid (ceil(max pages / 4), n_tab).
-__global__ void __launch_bounds__(128) prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
-    if (ctl->abort) return;
-    const int i = blockIdx.y;
+// One warp copies destination page j of launch table i.
+__device__ __forceinline__ void copy_page_warp(const DevState& s, const PrefillArgs& a, const LaunchCtl* ctl, int i,
+                                               int j) {
     const int lane = threadIdx.x & 31;
-    const int wid = threadIdx.x >> 5;
-    const int j = blockIdx.x * (blockDim.x >> 5) + wid;
     const int L = a.tab_len[i];
     const int keep = (s.policy == PE_POLICY_PAGED_EVICTION && L > s.C) ? s.C : L;
     const int B = s.B;
@@ -816,6 +820,108 @@ __global__ void __launch_bounds__(128) prefill_copy_kernel(DevState s, PrefillAr
         for (int u = 0; u < ns; ++u) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * u);
     }
     if (lane == 0 && (j + 1) * B <= keep) s.page_scores[page] = sum / static_cast<double>(B);
+}
+
+__global__ void __launch_bounds__(128) prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
+    if (ctl->abort) return;
+    copy_page_warp(s, a, ctl, blockIdx.y, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+}
+
+// ---------------------------------------------------------------------------
+// prefill_fused_kernel: the whole prune+pack of one call in ONE persistent
+// launch (one 1024-thread CTA per SM). CTAs take work items in schedule
+// order from a global counter:
+//   S(q, u)  score unit u of sequence q: tokens [u*T, u*T+T) x all heads
+//            (same arithmetic as prefill_score_kernel); then seq_done[q]++.
+//   X(q, h)  table (q, h): wait until every score unit of q is done, then the
+//            CTA select (select_table_cta) and the survivor copy (one warp per
+//            page), i.e. what prefill_select_cta_kernel + prefill_copy_kernel do.
+// The host schedule interleaves X(q) after S(q+1), so while some SMs run a
+// latency-bound select, the others keep streaming the next sequence's K/V:
+// the select no longer serialises with the HBM-bound passes. Deadlock-free:
+// an X item only waits for S items that precede it in the schedule, and
+// those were claimed by CTAs that are running.
+template <int SV>
+__global__ void __launch_bounds__(1024, 1) prefill_fused_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl,
+                                                                 const int32_t* items, int n_items, int* work_ctr,
+                                                                 int* seq_done, const int32_t* seq_units,
+                                                                 int unit_tokens) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int sh_item;
+    if (ctl->abort) return;
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    const int H = s.tab_heads;
+    for (;;) {
+        if (threadIdx.x == 0) sh_item = atomicAdd(work_ctr, 1);
+        __syncthreads();
+        const int id = sh_item;
+        __syncthreads();
+        if (id >= n_items) break;
+        const int d = __ldg(items + id);
+        const int sq = (d >> 16) & 0x7FFF;
+        const int idx = d & 0xFFFF;
+        if (d >= 0) {  // S: score unit
+            const int L = a.tab_len[sq * H];
+            const int tok_lo = idx * unit_tokens;
+            const int tok_hi = min(L, tok_lo + unit_tokens);
+            const int64_t f_lo = (int64_t)tok_lo * H, f_hi = (int64_t)tok_hi * H;
+            const int64_t row0 = a.tab_tok0[sq * H] * H;
+            const int64_t n_units = (f_hi - f_lo + 15) / 16;
+            for (int64_t u = wid; u < n_units; u += nw) {
+                const int64_t f = f_lo + u * 16 + (lane >> 1);
+                const bool valid = f < f_hi;
+                const int64_t off = (row0 + f) * s.row_bytes;
+                const double S = pair_token_score<SV>(a.k + off, a.v + off, valid, s.w, s.dtype);
+                if (valid && (lane & 1) == 0) {
+                    const int tok = static_cast<int>(f / H);
+                    const int h = static_cast<int>(f - (int64_t)tok * H);
+                    a.keys[a.tab_keybase[sq * H + h] + tok] = static_cast<unsigned long long>(__double_as_longlong(S));
+                }
+            }
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) atomicAdd(seq_done + sq, 1);
+        } else {  // X: select + copy of table (sq, idx)
+            if (threadIdx.x == 0) {
+                const int need = __ldg(seq_units + sq);
+                while (true) {
+                    int v;
+                    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(seq_done + sq) : "memory");
+                    if (v >= need) break;
+                    __nanosleep(200);
+                }
+            }
+            __syncthreads();
+            const int i = sq * H + idx;
+            select_table_cta(s, a, i, smem, ctl);
+            __threadfence();
+            __syncthreads();
+            const int L = a.tab_len[i];
+            const int keep = (s.policy == PE_POLICY_PAGED_EVICTION && L > s.C) ? s.C : L;
+            const int n_pages = (keep + s.B - 1) / s.B;
+            for (int j = wid; j < n_pages; j += nw) copy_page_warp(s, a, ctl, i, j);
+            __syncthreads();
+        }
+    }
+}
+
+void launch_prefill_fused_any(int variant, int grid, size_t smem, cudaStream_t st, const DevState& s,
+                              const PrefillArgs& a, const LaunchCtl* ctl, const int32_t* items, int n_items,
+                              int* work_ctr, int* seq_done, const int32_t* seq_units, int unit_tokens) {
+    PE_SCORE_DISPATCH(variant, (prefill_fused_kernel<SV><<<grid, 1024, smem, st>>>(
+                                   s, a, ctl, items, n_items, work_ctr, seq_done, seq_units, unit_tokens)));
+}
+
+const void* prefill_fused_fn(int variant) {
+    switch (variant) {
+    case kScoreBf16x16: return reinterpret_cast<const void*>(prefill_fused_kernel<kScoreBf16x16>);
+    case kScoreBf16x8: return reinterpret_cast<const void*>(prefill_fused_kernel<kScoreBf16x8>);
+    case kScoreF32x16: return reinterpret_cast<const void*>(prefill_fused_kernel<kScoreF32x16>);
+    case kScoreF32x32: return reinterpret_cast<const void*>(prefill_fused_kernel<kScoreF32x32>);
+    default: return reinterpret_cast<const void*>(prefill_fused_kernel<kScoreGeneric>);
+    }
 }
 
 }  // namespace pe

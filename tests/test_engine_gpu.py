@@ -90,8 +90,15 @@ def test_prefill_ties_across_cta_boundaries(select_path):
     np.testing.assert_array_equal(eng.retained_positions(0), np.arange(L - C, L))
 
 
+@pytest.fixture(params=["waves", "fused"])
+def prefill_variant(request, monkeypatch):
+    """The default multi-kernel wave pipeline and the opt-in persistent kernel."""
+    monkeypatch.setenv("PE_PREFILL_FUSED", "1" if request.param == "fused" else "0")
+    return request.param
+
+
 @pytest.mark.parametrize("gen", [random_kv, grid_kv])
-def test_prefill_long_tables_windowed_select(gen):
+def test_prefill_long_tables_windowed_select(gen, prefill_variant):
     """Tables of >= 8192 tokens take the sampled pivot window of the CTA
     select kernel (candidates only; tie-heavy grid data overflows the window
     and exercises the full-pass fallback). Bit-exact against the oracle."""
