@@ -323,6 +323,8 @@ __device__ __forceinline__ void split_bf16x2(float x0, float x1, uint32_t& hi, u
     lo = pack_bf16x2(x0 - h0, x1 - h1);
 }
 
+constexpr int kAttnMaxSplitPages = 512;
+
 template <int D>
 __global__ void __launch_bounds__(kAttnThreads, 2) attention_mma_kernel(DevState s, AttnArgs a) {
     constexpr int RB = D * 2;          // bf16 row bytes
@@ -370,10 +372,18 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_mma_kernel(DevState
 
     const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
     const int my_n = (p_end - p_begin) > wid ? ((p_end - p_begin) - wid + nw - 1) / nw : 0;
+    // this split's page ids, read once up front: the cp.async of page k must
+    // not wait for a dependent block-table load
+    __shared__ int32_t ids[kAttnMaxSplitPages];
+    const bool ids_sm = p_end - p_begin <= kAttnMaxSplitPages;
+    if (ids_sm)
+        for (int j = threadIdx.x; j < p_end - p_begin; j += blockDim.x) ids[j] = __ldg(row + p_begin + j);
+    __syncthreads();
     auto issue = [&](int k) {
         if (k < my_n) {
             const int pg = p_begin + wid + k * nw;
-            const uint8_t* base = s.pages + (int64_t)__ldg(row + pg) * 32 * RB;
+            const int32_t id = ids_sm ? ids[pg - p_begin] : __ldg(row + pg);
+            const uint8_t* base = s.pages + (int64_t)id * 32 * RB;
             uint8_t* st = stage + (k % NST) * PAGE_SM;
 #pragma unroll
             for (int x = lane; x < 32 * PIECES; x += 32) {
