@@ -276,7 +276,8 @@ def run_b200(args, cfg, world, rank, local):
     n_tab_layer = S * H
     k1_bytes = n_tab_layer * k1_bytes_per_table(L, C, row)
     pre_sorted = sorted(pre_ms[1:] or pre_ms)
-    prefill = {"kernel": "K1 prefill_prune_pack (cluster of 8 CTAs per table)",
+    prefill = {"kernel": "K1 prefill_prune_pack: score + CTA-per-table select + copy, "
+                         "4 sequence waves on 2 streams",
                "ms_per_layer_p50": round(statistics.median(pre_sorted), 4),
                "gbs": round(k1_bytes / (statistics.median(pre_sorted) * 1e-3) / 1e9, 1),
                "tables_per_layer": n_tab_layer,
@@ -295,7 +296,10 @@ def run_b200(args, cfg, world, rank, local):
     step_bytes = k2_alg + k0_alg
     k2_per_launch = (n_tab if args.evict_launch == "step" else n_tab_layer) * k2_bytes_per_table(C, row)
 
+    cycles = [0]  # eviction cycles run on every table (cadence check)
+
     def cycle(record=None, host=False, mode=pe.ScoreMode.RECOMPUTE, victims_host=None):
+        cycles[0] += 1
         for j in range(B):
             if host:
                 eng.append_token(0, NL, h_k[j], h_v[j], pos)
@@ -404,6 +408,7 @@ def run_b200(args, cfg, world, rank, local):
                 attn_ms.append((a, b))
         d1.record(stream)
         d1.synchronize()
+        cycles[0] += 1
         dec_ms = d0.elapsed_time(d1)
         at = [a.elapsed_time(b) for a, b in attn_ms]
         k3_bytes = n_tab_layer * k3_bytes_per_table(C + B // 2, row, G, d, elt)
@@ -413,6 +418,15 @@ def run_b200(args, cfg, world, rank, local):
                   "attention_gbs": round(k3_bytes / (statistics.median(at) * 1e-3) / 1e9, 1)}
 
     st = eng.stats()
+    # full-size parity by size-independent properties (untimed): every table
+    # evicted exactly once per 16-token cycle (policy.cpp:147-150 cadence) and
+    # the device invariant checker over all tables and the whole pool
+    inv = eng.check_invariants()
+    checks = {"evictions_expected": n_tab * cycles[0], "evictions_observed": int(st.pages_evicted),
+              "cadence_ok": int(st.pages_evicted) == n_tab * cycles[0],
+              "invariant_violations": inv["violations"], "tables_checked": inv["tables_checked"],
+              "pages_mapped_plus_free": inv["pages_mapped"] + inv["free_pages"],
+              "pool_capacity": int(eng.capacity)}
     ranks = gather_stats(RankStats(rank=rank, tables=n_tab, tokens_scored=int(st.tokens_scored),
                                    pages_evicted=int(st.pages_evicted),
                                    algorithmic_bytes=int(step_bytes * args.steps), kernel_ms=k2_ms))
@@ -443,6 +457,7 @@ def run_b200(args, cfg, world, rank, local):
             "prefill": prefill,
             "decode": decode,
             "e2e": e2e,
+            "checks": checks,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

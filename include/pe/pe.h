@@ -283,6 +283,25 @@ pe_status pe_read_page_holes(pe_engine* eng, int32_t page_begin, int32_t n_pages
 pe_status pe_prompt_select(int32_t device, int32_t rule, const float* keys, int32_t n, int32_t w,
                            const int64_t* positions, int32_t k, uint8_t* evicted_flags);
 
+/* Structural invariants of the whole engine state, checked on the device
+ * (selfcheck.cpp:19-75, test_policies.cpp:220-234,437-473):
+ * every non-newest page full and hole-free, retained == the occupied slots,
+ * PagedEviction retained <= C + B, positions strictly increasing in logical
+ * order, every page id either mapped exactly once or free exactly once
+ * (page conservation, allocated + free == capacity). Synchronous. */
+typedef struct pe_invariants {
+    int64_t tables_checked;
+    int64_t pages_mapped;
+    int64_t free_pages;
+    int64_t violations;          /* sum of the counts below */
+    int64_t page_not_full;       /* a non-newest page with holes                 */
+    int64_t retained_mismatch;   /* retained != occupied slots of the table      */
+    int64_t budget_violations;   /* PagedEviction engine: retained > C + B       */
+    int64_t position_order;      /* positions not strictly increasing            */
+    int64_t page_refcount;       /* page ids mapped/free != exactly once         */
+} pe_invariants;
+pe_status pe_check_invariants(pe_engine* eng, pe_invariants* out);
+
 /* One table's block-table row (page_ids [num_pages], nullable) and counters. */
 pe_status pe_read_table(pe_engine* eng, int32_t table, int32_t* page_ids, int32_t* num_pages,
                         int32_t* newest_fill, int32_t* retained);

@@ -34,6 +34,12 @@ class PeStats(C.Structure):
         "pages_evicted", "kernel_launches")]
 
 
+class PeInvariants(C.Structure):
+    _fields_ = [(n, c_i64) for n in (
+        "tables_checked", "pages_mapped", "free_pages", "violations", "page_not_full",
+        "retained_mismatch", "budget_violations", "position_order", "page_refcount")]
+
+
 class PeDeviceView(C.Structure):
     _fields_ = [("pages", c_vp), ("block_table", c_vp), ("num_pages", c_vp),
                 ("newest_fill", c_vp), ("retained", c_vp), ("positions", c_vp)]
@@ -71,6 +77,7 @@ SIGNATURES = {
     "pe_table_evict_token": (C.c_int, [c_vp, c_i32, c_i32, c_i64, c_i32, c_i64, c_vp, c_vp]),
     "pe_read_page_holes": (C.c_int, [c_vp, c_i32, c_i32, c_vp]),
     "pe_prompt_select": (C.c_int, [c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_i32, c_vp]),
+    "pe_check_invariants": (C.c_int, [c_vp, C.POINTER(PeInvariants)]),
 }
 
 

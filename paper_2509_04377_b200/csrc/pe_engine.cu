@@ -1109,6 +1109,47 @@ pe_status pe_read_page_holes(pe_engine* e, int32_t page_begin, int32_t n_pages, 
     return PE_OK;
 }
 
+pe_status pe_check_invariants(pe_engine* e, pe_invariants* out) {
+    if (e == nullptr || out == nullptr) return fail(PE_INVALID_ARG, "null argument");
+    const DevState& s = e->s;
+    cudaSetDevice(e->device);
+    int32_t* refs = nullptr;
+    unsigned long long* ctr = nullptr;
+    if (dalloc(&refs, (size_t)s.capacity) != cudaSuccess || dalloc(&ctr, 8) != cudaSuccess) {
+        cudaGetLastError();
+        if (refs) cudaFree(refs);
+        return fail(PE_CUDA_ERROR, "invariant scratch allocation failed");
+    }
+    cudaError_t ce = cudaMemset(refs, 0, sizeof(int32_t) * (size_t)s.capacity);
+    if (ce == cudaSuccess) ce = cudaMemset(ctr, 0, sizeof(unsigned long long) * 8);
+    if (ce == cudaSuccess) {
+        invariants_tables_kernel<<<(s.n_tables + 7) / 8, 256>>>(s, refs, ctr);
+        invariants_free_kernel<<<e->sm_count * 4, 256>>>(s, refs);
+        invariants_refs_kernel<<<e->sm_count * 4, 256>>>(s, refs, ctr);
+        ce = cudaGetLastError();
+    }
+    unsigned long long h[8] = {};
+    int32_t top = 0;
+    if (ce == cudaSuccess) ce = cudaMemcpy(h, ctr, sizeof(h), cudaMemcpyDeviceToHost);
+    if (ce == cudaSuccess) ce = cudaMemcpy(&top, s.top, sizeof(int32_t), cudaMemcpyDeviceToHost);
+    cudaFree(refs);
+    cudaFree(ctr);
+    if (ce != cudaSuccess) return fail(PE_CUDA_ERROR, std::string("invariant check: ") + cudaGetErrorString(ce));
+    e->stats.kernel_launches += 3;
+    std::memset(out, 0, sizeof(*out));
+    out->tables_checked = s.n_tables;
+    out->pages_mapped = (int64_t)h[0];
+    out->free_pages = top;
+    out->page_not_full = (int64_t)h[1];
+    out->retained_mismatch = (int64_t)h[2];
+    out->budget_violations = (int64_t)h[3];
+    out->position_order = (int64_t)h[4];
+    out->page_refcount = (int64_t)h[5];
+    out->violations = out->page_not_full + out->retained_mismatch + out->budget_violations + out->position_order +
+                      out->page_refcount;
+    return PE_OK;
+}
+
 pe_status pe_pool_allocate(pe_engine* e, int32_t* page_id) {
     if (e == nullptr || page_id == nullptr) return fail(PE_INVALID_ARG, "null argument");
     cudaSetDevice(e->device);

@@ -385,4 +385,85 @@ __global__ void flag_first_kernel(const int* sidx, int k, uint8_t* flags) {
     if (i < k) flags[sidx[i]] = 1;
 }
 
+
+// ---------------------------------------------------------------------------
+// Invariant checker (pe_check_invariants): one warp per table, then the free
+// stack, then a per-page reference count pass. counters: [0] pages mapped,
+// [1] page not full, [2] retained mismatch, [3] budget, [4] position order,
+// [5] refcount.
+__global__ void invariants_tables_kernel(DevState s, int32_t* refs, unsigned long long* counters) {
+    const int lane = threadIdx.x & 31;
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (t >= s.n_tables) return;
+    const int N = s.num_pages[t];
+    const int nf = s.newest_fill[t];
+    const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
+    int occupied = 0, not_full = 0, order = 0;
+    long long prev_last = -1;  // last retained position of the previous chunk of pages
+    for (int base = 0; base < N; base += 32) {
+        const int j = base + lane;
+        long long first = -1, last = -1;
+        int cnt = 0;
+        bool bad_order = false;
+        if (j < N) {
+            const int page = row[j];
+            atomicAdd(refs + page, 1);
+            const int cursor = j == N - 1 ? nf : s.B;
+            long long pv = -1;
+            for (int sl = 0; sl < cursor; ++sl) {
+                if (slot_hole(s, page, sl)) continue;
+                const long long p = s.positions[(int64_t)page * s.B + sl];
+                if (pv >= 0 && p <= pv) bad_order = true;
+                if (first < 0) first = p;
+                pv = p;
+                ++cnt;
+            }
+            last = pv;
+            if (j < N - 1 && cnt != s.B) ++not_full;
+        }
+        occupied += cnt;
+        order += bad_order;
+        // ordering across consecutive pages: page j's first > page j-1's last
+        const long long left_last = __shfl_up_sync(0xFFFFFFFFu, last, 1);
+        const long long chain = lane == 0 ? prev_last : left_last;
+        if (j < N && first >= 0 && chain >= 0 && first <= chain) ++order;
+        // carry the last non-empty page's last position into the next chunk
+        long long carry = last;
+        for (int o = 1; o < 32; o <<= 1) {  // inclusive "last valid" scan
+            const long long v = __shfl_up_sync(0xFFFFFFFFu, carry, o);
+            if (lane >= o && carry < 0) carry = v;
+        }
+        const long long chunk_last = __shfl_sync(0xFFFFFFFFu, carry, 31);
+        if (chunk_last >= 0) prev_last = chunk_last;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        occupied += __shfl_xor_sync(0xFFFFFFFFu, occupied, o);
+        not_full += __shfl_xor_sync(0xFFFFFFFFu, not_full, o);
+        order += __shfl_xor_sync(0xFFFFFFFFu, order, o);
+    }
+    if (lane == 0) {
+        atomicAdd(counters + 0, (unsigned long long)N);
+        if (not_full) atomicAdd(counters + 1, (unsigned long long)not_full);
+        if (occupied != s.retained[t]) atomicAdd(counters + 2, 1ull);
+        if (s.policy == PE_POLICY_PAGED_EVICTION && s.retained[t] > s.C + s.B) atomicAdd(counters + 3, 1ull);
+        if (order) atomicAdd(counters + 4, (unsigned long long)order);
+    }
+}
+
+__global__ void invariants_free_kernel(DevState s, int32_t* refs) {
+    const int top = *s.top;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < top; i += gridDim.x * blockDim.x) {
+        const int page = s.stack[i];
+        if (page >= 0 && page < s.capacity) atomicAdd(refs + page, 1);
+    }
+}
+
+__global__ void invariants_refs_kernel(DevState s, const int32_t* refs, unsigned long long* counters) {
+    unsigned long long bad = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.capacity; i += gridDim.x * blockDim.x)
+        bad += refs[i] != 1;
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xFFFFFFFFu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(counters + 5, bad);
+}
+
 }  // namespace pe

@@ -318,6 +318,14 @@ class PagedEvictionEngine:
         _check(self.lib.pe_get_stats(self.h, C.byref(out)))
         return out
 
+    def check_invariants(self) -> dict:
+        """Device-side structural invariants of every table and the pool
+        (pe_check_invariants; selfcheck.cpp:19-75): returns the counts,
+        `violations` == 0 when everything holds."""
+        out = _lib.PeInvariants()
+        _check(self.lib.pe_check_invariants(self.h, C.byref(out)))
+        return {name: int(getattr(out, name)) for name, _ in _lib.PeInvariants._fields_}
+
     def device_view(self) -> _lib.PeDeviceView:
         out = _lib.PeDeviceView()
         _check(self.lib.pe_get_device_view(self.h, C.byref(out)))

@@ -342,3 +342,35 @@ def test_prefill_long_context_cluster_select():
     _, oev = orc.prefill(0, k, v, cu)
     np.testing.assert_array_equal(ev, oev)
     check(eng, orc, "long: ")
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_invariants_hold_after_prefill_and_decode(mode):
+    """pe_check_invariants on a decoded engine: no violation, pages mapped +
+    free == capacity; then a corrupted block table is detected."""
+    rng = np.random.default_rng(77)
+    B, C, d, H = 16, 64, 128, 2
+    lens = np.array([300, 64, 17, 150])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=len(lens), n_layers=2, H=H, d=d, B=B, C=C, dtype=oracle.BF16)
+    for layer in range(2):
+        k, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+        v, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+        eng.prefill_compress(layer, dev(k), dev(v), cu)
+    pos = lens.astype(np.int64).copy()
+    for step in range(1, 3 * B + 1):
+        kk, _ = random_kv(rng, (2, len(lens), H, d), oracle.BF16)
+        vv, _ = random_kv(rng, (2, len(lens), H, d), oracle.BF16)
+        eng.decode_step(0, 2, dev(kk), dev(vv), torch.from_numpy(pos).cuda(), step, mode=mode)
+        pos += 1
+    eng.sync()
+    inv = eng.check_invariants()
+    assert inv["violations"] == 0, inv
+    assert inv["pages_mapped"] + inv["free_pages"] == eng.capacity
+    assert inv["tables_checked"] == eng.n_tables
+    # corrupt: release a page that table 0 still maps (a double owner)
+    bt, npg, _, _ = eng.tables()
+    pid = int(bt[0, 0])
+    assert eng.lib.pe_pool_release(eng.h, pid) == 0
+    bad = eng.check_invariants()
+    assert bad["page_refcount"] > 0 and bad["violations"] > 0, bad
