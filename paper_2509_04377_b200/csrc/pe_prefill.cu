@@ -516,8 +516,8 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
     constexpr int kSegCap = kSelHistCopies * 2048 / 32;
     if (sampled) {
         uint32_t* samp = hist;
-        samp[tid] = static_cast<uint32_t>(__ldcg(gk + (int)(((int64_t)tid * L) >> 10)) >> 32);
-        for (int k = 2; k <= 1024; k <<= 1) {
+        samp[tid] = static_cast<uint32_t>(__ldcg(gk + (int)(((int64_t)tid * L) / nthr)) >> 32);
+        for (int k = 2; k <= nthr; k <<= 1) {
             for (int j = k >> 1; j > 0; j >>= 1) {
                 __syncthreads();
                 const int o = tid ^ j;
@@ -531,10 +531,11 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
             }
         }
         __syncthreads();
-        const int r = (int)(((int64_t)E * 1024) / L);
-        const int lo_i = r - 40, hi_i = r + 40;
+        const int r = (int)(((int64_t)E * nthr) / L);
+        const int win = nthr / 32 + 8;  // ~3.5 sigma of the sample quantile
+        const int lo_i = r - win, hi_i = r + win;
         p_lo = lo_i <= 0 ? 0u : samp[lo_i];
-        p_hi = hi_i >= 1023 ? 0xFFFFFFFFu : samp[hi_i];
+        p_hi = hi_i >= nthr - 1 ? 0xFFFFFFFFu : samp[hi_i];
         __syncthreads();
     }
 
