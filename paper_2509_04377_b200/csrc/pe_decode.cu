@@ -86,35 +86,53 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
     const unsigned pop_mask = __ballot_sync(0xFFFFFFFFu, pop && q == 0);
     if (lane == 0) sh_warp_cnt[wid] = __popc(pop_mask);
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (wid == 0) {
         int local = 0;
         for (int w = 0; w < nw; ++w) local += sh_warp_cnt[w];
         const unsigned long long ep = static_cast<unsigned long long>(static_cast<unsigned>(epoch)) << 32;
         int prefix = 0;
         if (lid == 0) {
-            const int top = *s.top;
-            ctl->pop_base = top;
-            st_release_u64(lb_status, ep | kLbInc | static_cast<unsigned long long>(local));
-            st_release_i32(&ctl->ready, epoch);
-            sh_pop_base = top;
-        } else {
-            st_release_u64(lb_status + lid, ep | kLbAgg | static_cast<unsigned long long>(local));
-            for (int j = lid - 1; j >= 0;) {
-                const unsigned long long w = ld_acquire_u64(lb_status + j);
-                if ((w >> 32) != static_cast<unsigned>(epoch)) continue;  // predecessor not yet published
-                prefix += static_cast<int>(w & ((1ull << 30) - 1));
-                if (w & kLbInc) break;
-                --j;
+            if (lane == 0) {
+                const int top = *s.top;
+                ctl->pop_base = top;
+                st_release_u64(lb_status, ep | kLbInc | static_cast<unsigned long long>(local));
+                st_release_i32(&ctl->ready, epoch);
+                sh_pop_base = top;
             }
-            st_release_u64(lb_status + lid, ep | kLbInc | static_cast<unsigned long long>(prefix + local));
-            while (ld_acquire_i32(&ctl->ready) != epoch) __nanosleep(32);
-            sh_pop_base = ctl->pop_base;
+        } else {
+            if (lane == 0) st_release_u64(lb_status + lid, ep | kLbAgg | static_cast<unsigned long long>(local));
+            // warp-parallel look-back: lane l reads predecessor j - l; the window
+            // ends at the closest predecessor that has published its inclusive
+            // prefix (CTA 0 always has)
+            for (int j = lid - 1;; j -= 32) {
+                const int idx = j - lane;
+                unsigned long long w = 0;
+                if (idx >= 0) {
+                    do {
+                        w = ld_acquire_u64(lb_status + idx);
+                    } while ((w >> 32) != static_cast<unsigned>(epoch));  // not yet published
+                }
+                const unsigned inc_mask = __ballot_sync(0xFFFFFFFFu, idx >= 0 && (w & kLbInc));
+                const int stop = inc_mask ? __ffs(inc_mask) - 1 : 31;
+                int v = (idx >= 0 && lane <= stop) ? static_cast<int>(w & ((1ull << 30) - 1)) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+                prefix += v;
+                if (inc_mask) break;
+            }
+            if (lane == 0) {
+                st_release_u64(lb_status + lid, ep | kLbInc | static_cast<unsigned long long>(prefix + local));
+                while (ld_acquire_i32(&ctl->ready) != epoch) __nanosleep(32);
+                sh_pop_base = ctl->pop_base;
+            }
         }
-        if (lid == n_ctas - 1) {
-            const int total = prefix + local;
-            *s.top = sh_pop_base - min(total, sh_pop_base);
+        if (lane == 0) {
+            if (lid == n_ctas - 1) {
+                const int total = prefix + local;
+                *s.top = sh_pop_base - min(total, sh_pop_base);
+            }
+            sh_prefix = prefix;
         }
-        sh_prefix = prefix;
     }
     __syncthreads();
     // rank of this table's pop among the launch's pops (ascending table id);
