@@ -41,7 +41,7 @@
 #include <string_view>
 #include <vector>
 
-#include "pe/pe.h"
+#include "pe.h"
 
 namespace pagedevict {
 

@@ -44,7 +44,7 @@ using namespace pagedevict;
 
 namespace {
 
-// Status codes: same numbering as include/pe/pe.h (pe_status).
+// Status codes: same numbering as include/pe.h (pe_status).
 enum : int {
     RS_OK = 0,
     RS_ERROR = 1,

@@ -2,7 +2,7 @@
 
 The hot path — prefill prune+pack (K1), decode append (K0), decode block
 eviction (K2/K2c) and paged decode attention (K3) — runs in hand-written
-sm_100a CUDA behind the C-ABI in include/pe/pe.h (libpe_b200.so). This
+sm_100a CUDA behind the C-ABI in include/pe.h (libpe_b200.so). This
 package is the Python mirror of the reference's cache-manager interface over
 that C-ABI; it has no CPU fallback.
 """

@@ -36,7 +36,7 @@ def nvcc() -> str:
 
 
 def inputs() -> list[Path]:
-    return [CSRC / s for s in SOURCES] + [CSRC / h for h in HEADERS] + [ROOT / "include" / "pe" / "pe.h",
+    return [CSRC / s for s in SOURCES] + [CSRC / h for h in HEADERS] + [ROOT / "include" / "pe.h",
                                                                         Path(__file__)]
 
 

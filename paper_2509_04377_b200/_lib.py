@@ -1,4 +1,4 @@
-"""ctypes binding of include/pe/pe.h (libpe_b200.so).
+"""ctypes binding of include/pe.h (libpe_b200.so).
 
 Loading fails loudly: there is no CPU fallback for the PagedEviction hot path.
 """
@@ -45,7 +45,7 @@ class PeDeviceView(C.Structure):
                 ("newest_fill", c_vp), ("retained", c_vp), ("positions", c_vp)]
 
 
-# every symbol include/pe/pe.h declares, with its signature
+# every symbol include/pe.h declares, with its signature
 SIGNATURES = {
     "pe_abi_version": (c_i32, []),
     "pe_last_error": (C.c_char_p, []),

@@ -1,5 +1,5 @@
 // Implementation of the C++ façade (include/pe/pagedevict.hpp) over the
-// engine's C-ABI (include/pe/pe.h). Host code here only validates, stages
+// engine's C-ABI (include/pe.h). Host code here only validates, stages
 // the caller's vectors, synchronises and translates status codes; every
 // cache mutation, eviction decision, prefill selection and attention runs
 // in the engine's sm_100a kernels.

@@ -1,4 +1,4 @@
-// Host side of the C-ABI (include/pe/pe.h): engine lifecycle, argument
+// Host side of the C-ABI (include/pe.h): engine lifecycle, argument
 // validation (mirroring the reference's exceptions as pe_status codes),
 // host-buffer staging, and the launch sequences of K0/K1/K2/K3.
 #include <cuda_runtime.h>

@@ -12,7 +12,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "pe/pe.h"
+#include "pe.h"
 
 namespace pe {
 

@@ -7,7 +7,7 @@ Reference (proj/core/include/pagedevict/): PolicyKind / PolicyConfig
 (policy.hpp:95-120). The reference objects are per (sequence, layer) and
 mutated one token at a time; here ONE engine owns every table of a rank in
 HBM and each call is a batched, stream-ordered launch over many tables
-(include/pe/pe.h). Per-table accessors read the device state back.
+(include/pe.h). Per-table accessors read the device state back.
 
 Buffers may be torch tensors (CUDA or CPU) or numpy arrays; host buffers are
 staged by the C-ABI itself.

@@ -1,5 +1,5 @@
 """CPU-side checks of the drop-in boundary: the C-ABI library builds, loads
-without a GPU, exports every symbol include/pe/pe.h declares, and fails
+without a GPU, exports every symbol include/pe.h declares, and fails
 loudly (PE_NO_DEVICE) instead of falling back to the CPU."""
 import ctypes as C
 import re
@@ -8,7 +8,7 @@ from pathlib import Path
 import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
-HEADER = ROOT / "include" / "pe" / "pe.h"
+HEADER = ROOT / "include" / "pe.h"
 
 
 def declared_functions():
