@@ -416,6 +416,36 @@ def run_b200(args, cfg, world, rank, local):
                   "ms_per_token_all_layers": round(dec_ms / B, 4),
                   "attention_us_per_layer_p50": round(statistics.median(at) * 1e3, 2),
                   "attention_gbs": round(k3_bytes / (statistics.median(at) * 1e-3) / 1e9, 1)}
+        # the downstream win: the same attention over the UNPRUNED cache
+        # (FullCache, one layer: all L tokens of the batch, 8.6 GB at cfg3)
+        try:
+            fgeo = pe.EngineGeometry(n_seqs=S, n_layers=1, n_kv_heads=H, head_dim=d,
+                                     dtype=pe.DTYPE_BF16 if bf16 else pe.DTYPE_F32, device=local,
+                                     max_pages_per_table=(L + B - 1) // B + 1)
+            feng = pe.PagedEvictionEngine(fgeo, pe.PolicyConfig(cache_budget=C, page_size=B,
+                                                                kind=pe.PolicyKind.FullCache))
+            fk = torch.empty((S * L, H, d), dtype=tdt, device=dev).normal_(generator=gen)
+            feng.prefill_compress(0, fk, torch.empty_like(fk).normal_(generator=gen), cu)
+            del fk
+            fat = []
+            for _ in range(5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                feng.attend(0, q, out, QH)
+                b.record(stream)
+                fat.append((a, b))
+            torch.cuda.synchronize()
+            f_us = statistics.median([a.elapsed_time(b) for a, b in fat]) * 1e3
+            feng.close()
+            torch.cuda.empty_cache()
+            f_bytes = n_tab_layer * k3_bytes_per_table(L, row, G, d, elt)
+            p_us = statistics.median(at) * 1e3
+            decode["full_cache"] = {"attention_us_per_layer_p50": round(f_us, 2),
+                                    "attention_gbs": round(f_bytes / (f_us * 1e-6) / 1e9, 1),
+                                    "retained_tokens_per_table": L,
+                                    "attention_speedup_pruned": round(f_us / p_us, 2)}
+        except Exception as exc:  # pool for the unpruned layer does not fit: report why
+            decode["full_cache"] = {"unavailable": str(exc)[:200]}
 
     st = eng.stats()
     # full-size parity by size-independent properties (untimed): every table
