@@ -374,3 +374,63 @@ def test_invariants_hold_after_prefill_and_decode(mode):
     assert eng.lib.pe_pool_release(eng.h, pid) == 0
     bad = eng.check_invariants()
     assert bad["page_refcount"] > 0 and bad["violations"] > 0, bad
+
+
+@pytest.mark.slow
+def test_cfg3_full_layer_sampled_against_reference(reference):
+    """BASELINE config 3 at full size for one layer — Llama-3.1-8B KV geometry,
+    64 sequences x 32768 tokens x 8 KV heads, C=4096, B=16, bf16 — then 16
+    decode tokens (one block eviction per table). Six sampled tables are
+    replayed through the UNMODIFIED reference (oracle/_ref: PagePool /
+    BlockTable / make_policy(PagedEviction) / attend) on the same bytes:
+    retained positions after prefill and after decode, every eviction
+    decision, and the GQA attention output (<= 1e-3, bf16) must agree."""
+    import oracle
+
+    S, H, d, L, C, B, G = 64, 8, 128, 32768, 4096, 16, 4
+    eng, _ = None, None
+    geo = pe.EngineGeometry(n_seqs=S, n_layers=1, n_kv_heads=H, head_dim=d, dtype=oracle.BF16)
+    eng = pe.PagedEvictionEngine(geo, pe.PolicyConfig(cache_budget=C, page_size=B))
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+    k_in = torch.randn((S * L, H, d), generator=gen, device="cuda", dtype=torch.float32).to(torch.bfloat16)
+    v_in = torch.randn((S * L, H, d), generator=gen, device="cuda", dtype=torch.float32).to(torch.bfloat16)
+    cu = np.arange(S + 1, dtype=np.int32) * L
+    eng.prefill_compress(0, k_in, v_in, cu)
+    eng.sync()
+    samples = [(0, 0), (13, 5), (31, 7), (42, 2), (50, 6), (63, 3)]
+    ref = {}
+    for sq, h in samples:
+        sess = oracle.RefSession(reference, capacity=C // B + 2, page_size=B, budget=C, n_tables=1,
+                                 width=d, kind=0)
+        kk = k_in[sq * L:(sq + 1) * L, h].float().cpu().numpy()
+        vv = v_in[sq * L:(sq + 1) * L, h].float().cpu().numpy()
+        sess.prefill(0, kk, vv)
+        ref[(sq, h)] = sess
+        np.testing.assert_array_equal(eng.retained_positions(sq * H + h), sess.read_table(0, False)["positions"],
+                                      err_msg=f"prefill survivors of table {(sq, h)}")
+    del k_in, v_in
+    torch.cuda.empty_cache()
+    pos = torch.full((S,), L, dtype=torch.int64, device="cuda")
+    for step in range(1, B + 1):
+        rk = torch.randn((1, S, H, d), generator=gen, device="cuda", dtype=torch.float32).to(torch.bfloat16)
+        rv = torch.randn((1, S, H, d), generator=gen, device="cuda", dtype=torch.float32).to(torch.bfloat16)
+        vic = eng.decode_step(0, 1, rk, rv, pos, step, victims=True)
+        for (sq, h), sess in ref.items():
+            kind, idx = sess.decode_step(0, rk[0, sq, h].float().cpu().numpy(), rv[0, sq, h].float().cpu().numpy(),
+                                         L + step - 1, step)
+            want = idx if kind == 2 else -1
+            assert int(vic[sq * H + h]) == want, (step, sq, h, int(vic[sq * H + h]), kind, idx)
+        pos += 1
+    eng.sync()
+    assert eng.stats().pages_evicted == S * H  # one block per table
+    q = torch.randn((S, H * G, d), generator=gen, device="cuda", dtype=torch.float32).to(torch.bfloat16)
+    out = torch.empty((S, H * G, d), dtype=torch.float32, device="cuda")
+    eng.attend(0, q, out, H * G)
+    qf, of = q.float().cpu().numpy(), out.cpu().numpy()
+    o = oracle.Oracle()
+    for (sq, h), sess in ref.items():
+        np.testing.assert_array_equal(eng.retained_positions(sq * H + h), sess.read_table(0, False)["positions"])
+        for g in range(G):
+            want = sess.attend(0, qf[sq, h * G + g], 1, d)
+            assert o.output_deviation(of[sq, h * G + g], want) <= 1e-3
