@@ -201,7 +201,6 @@ pe_status check_launch(pe_engine* e, const char* what) {
     return PE_OK;
 }
 
-constexpr int kEvictPagesPerCta = 32;
 
 }  // namespace
 
@@ -658,9 +657,16 @@ pe_status launch_evict(pe_engine* e, const DevState& sc, const TableSet& ts, int
     // one launch: the grid's last CTA pushes the released pages in ascending
     // table id (no separate planner)
     if (mode == PE_SCORE_RECOMPUTE) {
-        // balanced chunks of <= kEvictPagesPerCta pages (257 pages -> 9 x 29)
-        const int chunks = (sc.max_pages + kEvictPagesPerCta - 1) / kEvictPagesPerCta;
+        // Pages per CTA: as many as possible (a CTA's warps stream their pages
+        // without draining; one CTA per table reaches 97 % of the HBM peak on
+        // an all-layer launch), but enough CTAs for ~6 waves on small launches
+        // (a per-layer launch of 512 tables gets 9 chunks of 29 pages).
+        const int min_chunks = (sc.max_pages + kMaxPagesPerCta - 1) / kMaxPagesPerCta;
+        const int target_ctas = 28 * e->sm_count;
+        int chunks = std::max(min_chunks, (target_ctas + n - 1) / n);
+        chunks = std::max(min_chunks, std::min(chunks, (sc.max_pages + 7) / 8));
         const int ppc = (sc.max_pages + chunks - 1) / chunks;
+        chunks = (sc.max_pages + ppc - 1) / ppc;
         e->grid_tickets += (unsigned long long)n;  // one completion ticket per table
         launch_evict_score_any(e->variant, dim3(n, chunks), kEvictThreads, st, sc, ts, ppc,
                                e->evict_scratch, e->tickets, e->vpage, vdst, e->grid_tickets - 1);

@@ -8,7 +8,7 @@ namespace pe {
 
 constexpr int kAppendThreads = 128;      // 4 warps x 16 tables
 constexpr int kEvictThreads = 128;       // 4 warps per CTA
-constexpr int kMaxPagesPerCta = 64;
+constexpr int kMaxPagesPerCta = 288;
 constexpr int kPrefillThreads = 128;     // score kernel: 4 warps per CTA
 constexpr int kScoreTokensPerCta = 256;  // tokens (x all heads) per score CTA
 constexpr int kPackThreads = 256;        // select kernel: 8 warps per CTA

@@ -1,6 +1,6 @@
 # A/B (eviction step only) of two builds, alternating, same box.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -k "decode or smoke or golden or facade or exhaust or invariants" 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -x -q -k "decode or smoke or golden or facade or exhaust or invariants or cfg3" 2>&1 | tail -1
 run() {
   PE_LIB=$2 timeout 300 python bench.py --no-cpu --no-decode --steps 20 > gpurun_out/ab3_$1.txt 2>&1
   python - "$1" <<'PY'
