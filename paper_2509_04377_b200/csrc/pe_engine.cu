@@ -776,7 +776,10 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
     e->n_pending = 0;
     pe_status r = as_device(e, q, (size_t)s.n_seqs * n_q_heads * s.row_bytes, st, &dq);
     if (r != PE_OK) return r;
-    int splits = std::max(1, (e->sm_count * 8 + n_tab - 1) / n_tab);
+    // as few splits as fill the GPU once (2 CTAs per SM): a CTA's warps stream
+    // their pages without draining, so long CTAs beat extra waves (cfg3: one
+    // split per table 181 us vs three 191 us)
+    int splits = std::max(1, (e->sm_count * 2 + n_tab - 1) / n_tab);
     if (const char* sv = std::getenv("PE_ATTN_SPLITS")) splits = std::max(1, std::atoi(sv));
     splits = std::min(splits, std::max(1, (s.max_pages + 3) / 4));
     const int pps = (s.max_pages + splits - 1) / splits;
