@@ -242,6 +242,16 @@ def run_b200(args, cfg, world, rank, local):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     peak, peak_kind = load_peaks()
+    # live HBM probe (untimed): K2 is read-only traffic, so its roofline is
+    # also reported against the streaming-read bandwidth of this GPU
+    import ctypes as _C
+
+    from paper_2509_04377_b200 import _lib as _pl
+
+    _rd, _cp = _C.c_double(0.0), _C.c_double(0.0)
+    probe_ok = _pl.load().pe_probe_hbm(local, 8 << 30, 5, _C.byref(_rd), _C.byref(_cp)) == 0
+    probe = {"read_gbs": round(_rd.value, 1), "kind": "256-bit streaming read of 8 GiB, best of 5 (pe_probe_hbm)"} \
+        if probe_ok else None
     bf16 = cfg["dtype"] == "bf16"
     tdt = torch.bfloat16 if bf16 else torch.float32
     elt = 2 if bf16 else 4
@@ -483,7 +493,9 @@ def run_b200(args, cfg, world, rank, local):
                          "traffic_source": "ncu dram__bytes_read+write per launch, profiles/*bench_launches*.csv",
                          "kernel": "K2 evict_score_kernel, " + ("one launch per decode step (all 32 layers)"
                                                                   if args.evict_launch == "step" else "per-layer launch"),
-                         "algorithmic_bytes_per_launch": k2_per_launch, "peak_kind": peak_kind},
+                         "algorithmic_bytes_per_launch": k2_per_launch, "peak_kind": peak_kind,
+                         "probe": probe,
+                         "frac_of_probe_read": round(k2_gbs / probe["read_gbs"], 4) if probe else None},
             "prefill": prefill,
             "decode": decode,
             "e2e": e2e,

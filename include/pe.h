@@ -302,6 +302,11 @@ typedef struct pe_invariants {
 } pe_invariants;
 pe_status pe_check_invariants(pe_engine* eng, pe_invariants* out);
 
+/* HBM roofline probe: best-of-iters streaming read and copy bandwidth (GB/s,
+ * bytes counted once per direction) over a `bytes` buffer (>= 64 MB; use
+ * more than L2) on `device`. Synchronous; allocates 2 x bytes. */
+pe_status pe_probe_hbm(int32_t device, int64_t bytes, int32_t iters, double* read_gbs, double* copy_gbs);
+
 /* One table's block-table row (page_ids [num_pages], nullable) and counters. */
 pe_status pe_read_table(pe_engine* eng, int32_t table, int32_t* page_ids, int32_t* num_pages,
                         int32_t* newest_fill, int32_t* retained);

@@ -1237,4 +1237,58 @@ pe_status pe_prompt_select(int32_t device, int32_t rule, const float* keys, int3
     return PE_OK;
 }
 
+// ------------------------------------------------------------------ HBM probe
+pe_status pe_probe_hbm(int32_t device, int64_t bytes, int32_t iters, double* read_gbs, double* copy_gbs) {
+    if (bytes < (int64_t)(64 << 20) || iters <= 0) return fail(PE_INVALID_ARG, "probe needs >= 64 MB and iters > 0");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(PE_NO_DEVICE, "no CUDA device");
+    }
+    PE_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    PE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const size_t n16 = (size_t)bytes / 32 * 2;  // multiple of 32 bytes
+    uint4 *a = nullptr, *b = nullptr;
+    unsigned long long* sink = nullptr;
+    if (cudaMalloc(&a, n16 * 16) != cudaSuccess || cudaMalloc(&b, n16 * 16) != cudaSuccess ||
+        cudaMalloc(&sink, 8) != cudaSuccess) {
+        cudaGetLastError();
+        if (a) cudaFree(a);
+        if (b) cudaFree(b);
+        return fail(PE_CUDA_ERROR, "probe allocation failed");
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaMemset(a, 0x5A, n16 * 16);
+    const int grid = sms * 16;
+    float best_r = 1e30f, best_c = 1e30f;
+    for (int it = 0; it < iters + 1; ++it) {  // first pass warms up
+        float ms = 0.f;
+        cudaEventRecord(e0);
+        probe_read_kernel<<<grid, 256>>>(a, n16, sink);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (it > 0) best_r = std::min(best_r, ms);
+        cudaEventRecord(e0);
+        probe_copy_kernel<<<grid, 256>>>(a, b, n16);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (it > 0) best_c = std::min(best_c, ms);
+    }
+    const cudaError_t ce = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(a);
+    cudaFree(b);
+    cudaFree(sink);
+    if (ce != cudaSuccess) return fail(PE_CUDA_ERROR, std::string("probe: ") + cudaGetErrorString(ce));
+    if (read_gbs) *read_gbs = (double)n16 * 16 / (best_r * 1e-3) / 1e9;
+    if (copy_gbs) *copy_gbs = 2.0 * (double)n16 * 16 / (best_c * 1e-3) / 1e9;
+    return PE_OK;
+}
+
 }  // extern "C"

@@ -87,5 +87,7 @@ __global__ void flag_first_kernel(const int* sidx, int k, uint8_t* flags);
 __global__ void invariants_tables_kernel(DevState s, int32_t* refs, unsigned long long* counters);
 __global__ void invariants_free_kernel(DevState s, int32_t* refs);
 __global__ void invariants_refs_kernel(DevState s, const int32_t* refs, unsigned long long* counters);
+__global__ void probe_read_kernel(const uint4* src, size_t n16, unsigned long long* sink);
+__global__ void probe_copy_kernel(const uint4* src, uint4* dst, size_t n16);
 
 }  // namespace pe

@@ -10,6 +10,7 @@
 //   table_clear_kernel     BlockTable::clear         block_table.cpp:72-78
 //   table_attend_kernel    attend / attend_detailed  attention.cpp:15-99
 #include "pe_kernels.cuh"
+#include "pe_score.cuh"
 
 namespace pe {
 
@@ -464,6 +465,30 @@ __global__ void invariants_refs_kernel(DevState s, const int32_t* refs, unsigned
         bad += refs[i] != 1;
     for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xFFFFFFFFu, bad, o);
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(counters + 5, bad);
+}
+
+
+// ---------------------------------------------------------------------------
+// HBM probe (pe_probe_hbm): streaming read (256-bit loads, reduced so the
+// loads are live) and copy over a buffer larger than L2, for the roofline
+// denominators of read-dominated kernels (K2 reads 34.5 GB and writes 43 MB).
+__global__ void probe_read_kernel(const uint4* __restrict__ src, size_t n16, unsigned long long* sink) {
+    unsigned long long acc = 0;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16 / 2; i += stride) {
+        u32x8 v;
+        asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]),
+              "=r"(v.w[7])
+            : "l"(src + 2 * i));
+        acc += v.w[0] ^ v.w[3] ^ v.w[5] ^ v.w[7];
+    }
+    if (acc == 0x1234567890ull) atomicAdd(sink, acc);  // never true for the probe data; keeps the loads
+}
+
+__global__ void probe_copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, size_t n16) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) dst[i] = __ldcs(src + i);
 }
 
 }  // namespace pe

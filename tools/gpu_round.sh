@@ -8,4 +8,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 python tools/launch_summary.py gpurun_out/bench_launches_round.csv
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"evict_score_kernel" -s 1 -c 1 -o gpurun_out/prof_round_k2 python bench.py --steps 1 --warmup 3 --no-cpu --no-decode > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"prefill_score_kernel|prefill_select_cta_kernel|prefill_copy_kernel" -s 3 -c 3 -o gpurun_out/prof_round_k1 python bench.py --steps 1 --warmup 3 --no-cpu --no-decode > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"attention_mma_kernel" -s 2 -c 1 -o gpurun_out/prof_round_k3 python bench.py --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"append_kernel" -s 40 -c 1 -o gpurun_out/prof_round_k0 python bench.py --steps 3 --warmup 3 --no-cpu --no-decode > /dev/null 2>&1
 ls -la gpurun_out/*.ncu-rep
