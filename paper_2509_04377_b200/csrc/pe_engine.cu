@@ -594,7 +594,9 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     // aux stream: while one wave is in its latency-bound select, the other
     // stream's HBM-bound score / copy kernels keep the memory system busy.
     // The canonical page reservation (plan) is made once for the whole call.
-    int waves = n_seqs >= 8 ? 4 : (n_seqs >= 2 ? 2 : 1);
+    // (the cluster select of long tables is kept out of the wave overlap: its
+    // 8-CTA clusters co-schedule badly next to another stream's kernels)
+    int waves = !use_cta_select ? 1 : (n_seqs >= 8 ? 4 : (n_seqs >= 2 ? 2 : 1));
     if (const char* wv = std::getenv("PE_PREFILL_WAVES")) waves = std::max(1, std::min(n_seqs, std::atoi(wv)));
     if (waves > 1) {
         PE_CUDA(cudaEventRecord(e->ev_fork, st));
