@@ -287,7 +287,7 @@ def run_b200(args, cfg, world, rank, local):
     k1_bytes = n_tab_layer * k1_bytes_per_table(L, C, row)
     pre_sorted = sorted(pre_ms[1:] or pre_ms)
     prefill = {"kernel": "K1 prefill_prune_pack: score + CTA-per-table select + copy, "
-                         "4 sequence waves on 2 streams",
+                         "2 sequence waves on 2 streams",
                "ms_per_layer_p50": round(statistics.median(pre_sorted), 4),
                "gbs": round(k1_bytes / (statistics.median(pre_sorted) * 1e-3) / 1e9, 1),
                "tables_per_layer": n_tab_layer,

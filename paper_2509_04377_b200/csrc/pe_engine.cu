@@ -521,6 +521,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     a.n_tab = n_tab;
     a.seq_begin = seq_begin;
     a.layer = layer;
+    a.score_tokens = kScoreTokensPerCta;
     // PE_SELECT=cluster forces the cluster kernel (tests exercise both paths)
     const char* sel_env = std::getenv("PE_SELECT");
     const bool force_cluster = sel_env != nullptr && std::strcmp(sel_env, "cluster") == 0;
@@ -590,13 +591,13 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
         }
         return PE_OK;
     }
-    // Sequence waves ping-pong between the caller's stream and the engine's
+    // Two sequence waves ping-pong between the caller's stream and the engine's
     // aux stream: while one wave is in its latency-bound select, the other
     // stream's HBM-bound score / copy kernels keep the memory system busy.
     // The canonical page reservation (plan) is made once for the whole call.
     // (the cluster select of long tables is kept out of the wave overlap: its
     // 8-CTA clusters co-schedule badly next to another stream's kernels)
-    int waves = !use_cta_select ? 1 : (n_seqs >= 8 ? 4 : (n_seqs >= 2 ? 2 : 1));
+    int waves = !use_cta_select ? 1 : (n_seqs >= 2 ? 2 : 1);
     if (const char* wv = std::getenv("PE_PREFILL_WAVES")) waves = std::max(1, std::min(n_seqs, std::atoi(wv)));
     if (waves > 1) {
         PE_CUDA(cudaEventRecord(e->ev_fork, st));
@@ -616,7 +617,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
         if (aw.evicted_counts) aw.evicted_counts += q0 * H;
         aw.seq_begin = seq_begin + q0;
         aw.n_tab = (q1 - q0) * H;
-        launch_prefill_score_any(e->variant, dim3((max_len + kScoreTokensPerCta - 1) / kScoreTokensPerCta, q1 - q0),
+        launch_prefill_score_any(e->variant, dim3((max_len + aw.score_tokens - 1) / aw.score_tokens, q1 - q0),
                                  sw, s, aw, e->ctl);
         if (use_cta_select) {
             // one CTA per table, high key words in shared memory (no cluster barriers)

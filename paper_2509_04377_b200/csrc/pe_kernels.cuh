@@ -10,7 +10,7 @@ constexpr int kAppendThreads = 128;      // 4 warps x 16 tables
 constexpr int kEvictThreads = 128;       // 4 warps per CTA
 constexpr int kMaxPagesPerCta = 288;
 constexpr int kPrefillThreads = 128;     // score kernel: 4 warps per CTA
-constexpr int kScoreTokensPerCta = 256;  // tokens (x all heads) per score CTA
+constexpr int kScoreTokensPerCta = 64;   // tokens (x all heads) per score CTA (small CTAs balance best)
 constexpr int kPackThreads = 256;        // select kernel: 8 warps per CTA
 constexpr int kPrefillCluster = 8;       // CTAs per table (portable cluster size)
 
@@ -28,6 +28,7 @@ struct PrefillArgs {
     int32_t n_tab;
     int32_t seq_begin, layer;
     int32_t chunk_cap;                   // max tokens per CTA (keys smem capacity)
+    int32_t score_tokens;                // tokens (x all heads) per score CTA
 };
 
 __global__ void evict_cached_kernel(DevState s, TableSet ts, double* scratch, int32_t* vpage, int32_t* victims,

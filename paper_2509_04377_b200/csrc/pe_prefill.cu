@@ -83,9 +83,9 @@ __global__ void __launch_bounds__(kPrefillThreads) prefill_score_kernel(DevState
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
-    const int tok_lo = blockIdx.x * kScoreTokensPerCta;
+    const int tok_lo = blockIdx.x * a.score_tokens;
     if (tok_lo >= L) return;
-    const int tok_hi = min(L, tok_lo + kScoreTokensPerCta);
+    const int tok_hi = min(L, tok_lo + a.score_tokens);
     const int64_t f_lo = (int64_t)tok_lo * H;
     const int64_t f_hi = (int64_t)tok_hi * H;
     const int64_t row0 = a.tab_tok0[sq * H] * H;  // first (token, head) row of the sequence
