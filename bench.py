@@ -386,11 +386,11 @@ def run_b200(args, cfg, world, rank, local):
     eng.sync()
     barrier()
     w0 = time.perf_counter()
-    for _ in range(max(1, args.steps // 2)):
+    for _ in range(max(1, args.steps)):
         cycle(host=True, victims_host=vict_host)
     eng.sync()
     barrier()
-    e2e_s = max_over_ranks((time.perf_counter() - w0) / max(1, args.steps // 2))
+    e2e_s = max_over_ranks((time.perf_counter() - w0) / max(1, args.steps))
     e2e = {"value": round(world * step_bytes / e2e_s / 1e9, 3), "unit": "GB/s",
            "h2d_bytes_per_step": int(B * 2 * NL * S * H * d * elt + B * S * 8),
            "d2h_bytes_per_step": int(n_tab * 4),
