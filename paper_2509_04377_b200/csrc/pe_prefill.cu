@@ -444,13 +444,11 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackT
 // several keys, their low words (read from global memory, only for those
 // keys) are resolved with further passes. Then one position-order sweep
 // (block scans) emits the survivors. Same decisions as the cluster kernel.
-__device__ __forceinline__ void reduce_hist_copies(const uint32_t* copies, uint32_t* out, int nbins) {
+__device__ __forceinline__ void reduce_hist_copies(const uint32_t* copies, uint32_t* out, int nbins, int ncopies) {
     for (int b = threadIdx.x; b < 2048; b += blockDim.x) {
         uint32_t acc = 0;
-        if (b < nbins) {
-#pragma unroll
-            for (int c = 0; c < kSelHistCopies; ++c) acc += copies[c * 2048 + b];
-        }
+        if (b < nbins)
+            for (int c = 0; c < ncopies; ++c) acc += copies[c * 2048 + b];
         out[b] = acc;
     }
     __syncthreads();
@@ -516,20 +514,28 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
     constexpr int kSegCap = kSelHistCopies * 2048 / 32;
     if (sampled) {
         uint32_t* samp = hist;
-        samp[tid] = static_cast<uint32_t>(__ldcg(gk + (int)(((int64_t)tid * L) / nthr)) >> 32);
+        // bitonic sort of one sample per thread: partner distances >= 32 go
+        // through shared memory (15 barrier stages for 1024), shorter ones are
+        // warp shuffles on the value held in a register
+        uint32_t x = static_cast<uint32_t>(__ldcg(gk + (int)(((int64_t)tid * L) / nthr)) >> 32);
         for (int k = 2; k <= nthr; k <<= 1) {
             for (int j = k >> 1; j > 0; j >>= 1) {
-                __syncthreads();
-                const int o = tid ^ j;
-                if (o > tid) {
-                    const uint32_t x = samp[tid], y = samp[o];
-                    if ((x > y) == ((tid & k) == 0)) {
-                        samp[tid] = y;
-                        samp[o] = x;
-                    }
+                const bool up = (tid & k) == 0;
+                if (j >= 32) {
+                    samp[tid] = x;
+                    __syncthreads();
+                    const uint32_t y = samp[tid ^ j];
+                    __syncthreads();
+                    const bool lower = (tid & j) == 0;
+                    x = (lower == up) ? min(x, y) : max(x, y);
+                } else {
+                    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+                    const bool lower = (tid & j) == 0;
+                    x = (lower == up) ? min(x, y) : max(x, y);
                 }
             }
         }
+        samp[tid] = x;
         __syncthreads();
         const int r = (int)(((int64_t)E * nthr) / L);
         const int win = nthr / 32 + 8;  // ~3.5 sigma of the sample quantile
@@ -543,17 +549,21 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
     unsigned int hmin = 0xFFFFFFFFu, hmax = 0u;
     int n_below = 0, seg_n = 0;
     const int lane_id = tid & 31, warp_id = tid >> 5;
-    for (int j0 = tid - lane_id; j0 < L; j0 += 8 * nthr) {  // 8 independent loads in flight per thread
+    // warp w loads the position span the sweeps give it ([w*span, (w+1)*span)),
+    // so its below-window count is already the sweep's per-warp "less" count
+    const int wspan = sweep_span(L);
+    const int w_beg = min(L, warp_id * wspan), w_end = min(L, w_beg + wspan);
+    for (int j0 = w_beg; j0 < w_end; j0 += 8 * 32) {  // 8 independent loads in flight per thread
         unsigned long long kv[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const int j = j0 + lane_id + u * nthr;
-            kv[u] = j < L ? __ldcs(gk + j) : 0ull;
+            const int j = j0 + u * 32 + lane_id;
+            kv[u] = j < w_end ? __ldcs(gk + j) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const int j = j0 + lane_id + u * nthr;
-            const bool in = j < L;
+            const int j = j0 + u * 32 + lane_id;
+            const bool in = j < w_end;
             const uint32_t w = static_cast<uint32_t>(kv[u] >> 32);
             if (in) {
                 hi[j] = w;
@@ -576,7 +586,7 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
         hmax = max(hmax, __shfl_xor_sync(0xFFFFFFFFu, hmax, o));
         n_below += __shfl_xor_sync(0xFFFFFFFFu, n_below, o);
     }
-    __shared__ int w_below[32], w_seg[32], win_ok, n_cand;
+    __shared__ int w_below[32], w_seg[32], win_ok, n_cand, below_sum;
     if (tid == 0) {
         mm[0] = 0xFFFFFFFFu;
         mm[1] = 0u;
@@ -599,11 +609,11 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
                 c += w_seg[w];
             }
             win_ok = !over && c <= kSelCandCap && b < E && E <= b + c;
-            w_below[0] = b;
+            below_sum = b;
             n_cand = c;
         }
         __syncthreads();
-        below_total = w_below[0];
+        below_total = below_sum;
         if (win_ok) {
             // contiguous candidate list (warp segments in warp order)
             int off = 0;
@@ -642,17 +652,20 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
             const int bits = min(11, bitpos);
             const int shift = bitpos - bits;
             const unsigned int dmask = (1u << bits) - 1u;
-            for (int b = tid; b < kSelHistCopies * 2048; b += nthr) hcopy[b] = 0;
+            // candidate passes are small and spread out: one histogram copy
+            const int ncopies = use_cand ? 1 : kSelHistCopies;
+            uint32_t* hh = use_cand ? hcopy : my_hist;
+            for (int b = tid; b < ncopies * 2048; b += nthr) hcopy[b] = 0;
             __syncthreads();
             const int n_iter = use_cand ? (n_cand + nthr - 1) / nthr * nthr : n_round_all;
             for (int x = tid; x < n_iter; x += nthr) {
                 const int j = use_cand ? (x < n_cand ? cand[x] : L) : x;
                 const unsigned int w = j < L ? hi[j] : 0u;
                 const bool act = j < L && (bitpos == 32 || (w >> bitpos) == hp);
-                hist_add(my_hist, (w >> shift) & dmask, act);
+                hist_add(hh, (w >> shift) & dmask, act);
             }
             __syncthreads();
-            reduce_hist_copies(hcopy, hist, 1 << bits);
+            reduce_hist_copies(hcopy, hist, 1 << bits, ncopies);
             const int d = block_find_digit(hist, 1 << bits, k_rem, bc, scan_sm);
             k_rem -= bc[1];
             hp = (bitpos == 32 ? 0u : (hp << bits)) | static_cast<unsigned int>(d);
@@ -686,7 +699,9 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
                 const int bits = min(11, lbit);
                 const int shift = lbit - bits;
                 const unsigned int dmask = (1u << bits) - 1u;
-                for (int b = tid; b < kSelHistCopies * 2048; b += nthr) hcopy[b] = 0;
+                const int ncopies = use_cand ? 1 : kSelHistCopies;
+                uint32_t* hh = use_cand ? hcopy : my_hist;
+                for (int b = tid; b < ncopies * 2048; b += nthr) hcopy[b] = 0;
                 __syncthreads();
                 const int n_iter = use_cand ? (n_cand + nthr - 1) / nthr * nthr : n_round_all;
                 for (int x = tid; x < n_iter; x += nthr) {
@@ -697,10 +712,10 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
                         lw = static_cast<unsigned int>(__ldcg(gk + j));
                         act = (lbit == 32) || (lw >> lbit) == lp;
                     }
-                    hist_add(my_hist, (lw >> shift) & dmask, act);
+                    hist_add(hh, (lw >> shift) & dmask, act);
                 }
                 __syncthreads();
-                reduce_hist_copies(hcopy, hist, 1 << bits);
+                reduce_hist_copies(hcopy, hist, 1 << bits, ncopies);
                 const int d = block_find_digit(hist, 1 << bits, k_rem, bc, scan_sm);
                 k_rem -= bc[1];
                 lp = (lbit == 32 ? 0u : (lp << bits)) | static_cast<unsigned int>(d);
@@ -741,7 +756,25 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
             }
         }
     };
-    sweep_count(L, classify, w_less, w_tie);
+    if (windowed) {
+        // per-warp (less, tie) counts without a counting sweep: the load pass
+        // counted each warp's keys below the window; only the candidates need
+        // the threshold
+        if (tid < (nthr >> 5)) {
+            w_less[tid] = w_below[tid];
+            w_tie[tid] = 0;
+        }
+        __syncthreads();
+        for (int x = tid; x < n_cand; x += nthr) {
+            const int j = cand[x];
+            bool l = false, t = false;
+            classify(j, l, t);
+            if (l) atomicAdd(&w_less[j / wspan], 1);
+            if (t) atomicAdd(&w_tie[j / wspan], 1);
+        }
+    } else {
+        sweep_count(L, classify, w_less, w_tie);
+    }
     __syncthreads();
     if (tid == 0) sweep_bases(L, k_rem, 0, 0, w_less, w_tie, w_tieb, w_keepb);
     __syncthreads();
