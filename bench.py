@@ -321,6 +321,10 @@ def run_b200(args, cfg, world, rank, local):
             vh = victims_host[: nl * n_tab_layer] if victims_host is not None else None
             if record is not None:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                if mode == pe.ScoreMode.CACHED:
+                    # a ~50 us launch: keep the GPU busy so the event pair brackets
+                    # device time, not the host's launch latency
+                    torch.cuda._sleep(200_000)
                 a.record(stream)
                 eng.evict(l0, nl, step=0, mode=mode, victims=vh)
                 b.record(stream)

@@ -262,20 +262,28 @@ __device__ __forceinline__ void push_victims_if_last(const DevState& s, int n, i
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    const int per = (n + blockDim.x - 1) / blockDim.x;
-    const int lo = min(n, (int)threadIdx.x * per);
-    const int hi = min(n, lo + per);
-    int cnt = 0;
-    for (int i = lo; i < hi; ++i) cnt += __ldcg(vpage + i) >= 0;
-    int total;
-    int k = block_excl_scan(cnt, scan_sm, &total);
+    // tiles of 16 consecutive entries per thread: independent loads, one
+    // block scan per tile (ascending table id = canonical push order)
     const int top = *s.top;
-    for (int i = lo; i < hi; ++i) {
-        const int pg = __ldcg(vpage + i);
-        if (pg >= 0) s.stack[top + k++] = pg;
+    int base = 0;
+    for (int t0 = 0; t0 < n; t0 += blockDim.x * 16) {
+        const int i0 = t0 + threadIdx.x * 16;
+        int v[16];
+        int cnt = 0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            v[u] = (i0 + u < n) ? __ldcg(vpage + i0 + u) : -1;
+            cnt += v[u] >= 0;
+        }
+        int total;
+        int k = base + block_excl_scan(cnt, scan_sm, &total);
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (v[u] >= 0) s.stack[top + k++] = v[u];
+        base += total;
     }
     __syncthreads();
-    if (threadIdx.x == 0) *s.top = top + total;
+    if (threadIdx.x == 0) *s.top = top + base;
 }
 
 // ---------------------------------------------------------------------------
@@ -419,6 +427,69 @@ void launch_append_any(int variant, int blocks, cudaStream_t st, const DevState&
 // evict_cached_kernel (K2c): one warp per launch table; page means were
 // cached when each page filled, so the decision reads N doubles (gathered
 // through the block table) instead of N pages. Bit-identical to K2.
+// Tables of up to 32*KR pages are handled in registers: the block-table row
+// and the page means are loaded with two independent load levels, the argmin
+// is a shuffle reduction, and free_page's left shift of the row is done with
+// shuffles of the row held in registers (no dependent load chains).
+template <int KR>
+__device__ __forceinline__ void cached_evict_regs(const DevState& s, int t, int y, int32_t* vpage, int32_t* victims) {
+    const int lane = threadIdx.x & 31;
+    const int N = s.num_pages[t];
+    int32_t* row = s.block_table + (int64_t)t * s.max_pages;
+    int ids[KR];
+    double sc[KR];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) ids[k] = (lane + 32 * k < N) ? row[lane + 32 * k] : -1;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) sc[k] = ids[k] >= 0 ? __ldcg(s.page_scores + ids[k]) : 0.0;
+    // rank_pages (importance.cpp:62-75): strict <, ties -> smaller logical index
+    double best = 0.0;
+    int bj = 0x7FFFFFFF;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+        if (ids[k] >= 0 && (bj == 0x7FFFFFFF || sc[k] < best)) {
+            best = sc[k];
+            bj = lane + 32 * k;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+        const int oj = __shfl_xor_sync(0xFFFFFFFFu, bj, o);
+        if (oj != 0x7FFFFFFF && (bj == 0x7FFFFFFF || ob < best || (ob == best && oj < bj))) {
+            best = ob;
+            bj = oj;
+        }
+    }
+    const int victim = bj;
+    int victim_page = 0;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+        const int v = __shfl_sync(0xFFFFFFFFu, ids[k], victim & 31);
+        if (k == (victim >> 5)) victim_page = v;
+    }
+    // free_page (block_table.cpp:21-31): entries after the victim move one left
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+        const int nxt_same = __shfl_down_sync(0xFFFFFFFFu, ids[k], 1);
+        const int nxt_wrap = k + 1 < KR ? __shfl_sync(0xFFFFFFFFu, ids[k + 1 < KR ? k + 1 : k], 0) : -1;
+        const int nxt = lane < 31 ? nxt_same : nxt_wrap;
+        const int j = lane + 32 * k;
+        if (j >= victim && j < N - 1) row[j] = nxt;
+    }
+    if (lane == 0) {
+        row[N - 1] = -1;
+        s.num_pages[t] = N - 1;
+        s.retained[t] -= page_fill(s, victim_page, s.B);
+        if (s.holes_on) s.holes[victim_page] = 0ull;
+        s.newest_fill[t] = (N - 1 > 0) ? s.B : 0;
+        vpage[y] = victim_page;
+        if (victims) victims[y] = victim;
+        atomicAdd(s.evict_count, 1ull);
+    }
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(256) evict_cached_kernel(DevState s, TableSet ts, double* scratch,
                                                            int32_t* vpage, int32_t* victims,
                                                            unsigned long long grid_last) {
@@ -433,6 +504,10 @@ __global__ void __launch_bounds__(256) evict_cached_kernel(DevState s, TableSet 
                 vpage[y] = -1;
                 if (victims) victims[y] = -1;
             }
+        } else if (s.max_pages <= 32 * 9) {
+            cached_evict_regs<9>(s, t, y, vpage, victims);
+        } else if (s.max_pages <= 32 * 16) {
+            cached_evict_regs<16>(s, t, y, vpage, victims);
         } else {
             const int N = s.num_pages[t];
             const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
