@@ -434,3 +434,16 @@ def test_cfg3_full_layer_sampled_against_reference(reference):
         for g in range(G):
             want = sess.attend(0, qf[sq, h * G + g], 1, d)
             assert o.output_deviation(of[sq, h * G + g], want) <= 1e-3
+
+
+def test_hbm_probe_is_plausible():
+    """pe_probe_hbm: the streaming-read and copy bandwidths the bench reports
+    beside the roofline are in the B200's physical range."""
+    import ctypes
+
+    from paper_2509_04377_b200 import _lib
+
+    rd, cp = ctypes.c_double(), ctypes.c_double()
+    assert _lib.load().pe_probe_hbm(0, 1 << 30, 3, ctypes.byref(rd), ctypes.byref(cp)) == 0
+    assert 3000 < rd.value < 9000, rd.value
+    assert 2000 < cp.value < 9000, cp.value
