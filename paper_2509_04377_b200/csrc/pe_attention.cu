@@ -496,6 +496,10 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_mma_kernel(DevState
             ll += wpart_ml[(w2 * G + gg) * 2 + 1] * c;
             oo += wpart_o[(w2 * G + gg) * D + (xi % D)] * c;
         }
+        if (n_splits == 1) {  // the whole table: write the output directly
+            a.out[((int64_t)seq * a.n_q_heads + h * G + gg) * D + (xi % D)] = oo / ll;
+            continue;
+        }
         const int64_t pidx = ((int64_t)i * n_splits + sp) * G + gg;
         a.part_o[pidx * D + (xi % D)] = oo;
         if (xi % D == 0) {
@@ -503,7 +507,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_mma_kernel(DevState
             a.part_ml[pidx * 2 + 1] = ll;
         }
     }
-    merge_if_last(s, a, i, D);
+    if (n_splits > 1) merge_if_last(s, a, i, D);
 }
 
 size_t attention_mma_smem(int d, int G) {
