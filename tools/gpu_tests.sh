@@ -1,2 +1,2 @@
-timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -5
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.txt 2>&1; tail -3 gpurun_out/gpu_tests.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
