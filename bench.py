@@ -217,7 +217,7 @@ def cpu_baseline(cfg, args):
                 "sample": f"unavailable: {exc}"}
     threads = os.cpu_count() or 1
     tables = args.ref_tables or 1024
-    cycles = 64
+    cycles = 256
     row_alg = 2 * cfg["d"] * (2 if cfg["dtype"] == "bf16" else 4)
     secs, ev = ref.bench_decode_cycles(tables, cfg["C"], B, cfg["d"], threads, cycles, seed=7,
                                        warmup_cycles=1)
