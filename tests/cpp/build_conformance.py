@@ -83,9 +83,23 @@ def build_all() -> None:
     build_facade_tests()
     build_reference_conformance()
     build_scenario()
+    build_examples()
 
 
 if __name__ == "__main__":
     sys.path.insert(0, str(ROOT))
     build_all()
     print("built", sorted(p.name for p in OUT.iterdir()))
+
+
+def build_examples() -> Path:
+    """examples/decode_loop.cpp: the batched C-ABI driven from C++ host code."""
+    OUT.mkdir(parents=True, exist_ok=True)
+    out = OUT / "decode_loop"
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", "-I/usr/local/cuda/include",
+           str(ROOT / "examples" / "decode_loop.cpp"), f"-L{LIB_DIR}", "-lpe_b200", "-L/usr/local/cuda/lib64",
+           "-lcudart", f"-Wl,-rpath,{LIB_DIR}", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", str(out)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"g++ failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stderr[-4000:]}")
+    return out

@@ -87,3 +87,21 @@ def test_same_program_reference_vs_b200():
         assert kx[:-1] == ky[:-1]
         a, b = float(kx[-1]), float(ky[-1])
         assert abs(a - b) <= 1e-12 * max(abs(a), 1e-30) + 1e-30, (x, y)
+
+
+@pytest.mark.gpu
+def test_cpp_decode_loop_example():
+    """examples/decode_loop.cpp — the simulator's batched loop as C++ host code
+    over the C-ABI (prefill, eviction cycles, attention) at a reduced config:
+    one page eviction per table per cycle, no invariant violation."""
+    import json
+
+    binary = BUILD / "decode_loop"
+    if not binary.exists():
+        pytest.skip("decode_loop not built (tests/cpp/build_conformance.py)")
+    res = subprocess.run([str(binary), "8", "4", "8", "128", "8192", "1024", "2"], capture_output=True,
+                         text=True, timeout=600)
+    assert res.returncode == 0, res.stdout + res.stderr
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    assert line["invariant_violations"] == 0 and line["outputs_finite"] is True
+    assert line["pages_evicted"] == 8 * 4 * 8 * 3
