@@ -296,7 +296,16 @@ def run_b200(args, cfg, world, rank, local):
     prefill["frac"] = round(prefill["gbs"] / peak, 4)
 
     # ---------------- decode inputs: B tokens of rows for every table (device + pinned host)
-    pos = torch.full((S,), L, dtype=torch.int64, device=dev)
+    # every decode token's positions, precomputed (no per-token increment kernel)
+    max_tokens = B * (2 * args.steps + args.warmup + 16)
+    pos_all = (L + torch.arange(max_tokens, device=dev, dtype=torch.int64)).unsqueeze(1).expand(
+        max_tokens, S).contiguous()
+    tok = [0]
+
+    def next_pos():
+        p = pos_all[tok[0]]
+        tok[0] += 1
+        return p
     rows_k = torch.randn((B, NL, S, H, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
     rows_v = torch.randn((B, NL, S, H, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
     h_k = rows_k.cpu().pin_memory()
@@ -313,10 +322,9 @@ def run_b200(args, cfg, world, rank, local):
         cycles[0] += 1
         for j in range(B):
             if host:
-                eng.append_token(0, NL, h_k[j], h_v[j], pos)
+                eng.append_token(0, NL, h_k[j], h_v[j], next_pos())
             else:
-                eng.append_token(0, NL, rows_k[j], rows_v[j], pos)
-            pos.add_(1)
+                eng.append_token(0, NL, rows_k[j], rows_v[j], next_pos())
         spans = [(0, NL)] if args.evict_launch == "step" else [(layer, 1) for layer in range(NL)]
         for l0, nl in spans:
             vh = victims_host[: nl * n_tab_layer] if victims_host is not None else None
@@ -411,8 +419,7 @@ def run_b200(args, cfg, world, rank, local):
         d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d0.record(stream)
         for j in range(B):
-            eng.append_token(0, NL, rows_k[j], rows_v[j], pos)
-            pos.add_(1)
+            eng.append_token(0, NL, rows_k[j], rows_v[j], next_pos())
             for layer in range(NL):
                 if j == B - 1:
                     eng.evict(layer, 1)
