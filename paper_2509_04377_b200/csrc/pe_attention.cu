@@ -15,6 +15,7 @@
 // log2e folded into the scale) and accumulates P.V with one lane per
 // d/32-dimension slice. Warp and split partials are merged with the usual
 // (max, sum) log-sum-exp rescaling.
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include "pe_kernels.cuh"
@@ -523,6 +524,225 @@ void launch_attention_mma(int d, dim3 grid, size_t smem, cudaStream_t st, const 
 const void* attention_mma_fn(int d) {
     return d == 128 ? reinterpret_cast<const void*>(attention_mma_kernel<128>)
                     : reinterpret_cast<const void*>(attention_mma_kernel<64>);
+}
+
+
+// ---------------------------------------------------------------------------
+// TMA variant (bf16, d in {64, 128}, B = 16; the default): the same per-warp pipeline and math as
+// attention_mma_kernel, but each page is staged by two 2-D tensor-map loads
+// (cp.async.bulk.tensor, 64 columns x 32 rows each, SWIZZLE_128B) issued by
+// one lane and completing on the stage's mbarrier, instead of 512 16-byte
+// cp.async per page; ldmatrix addresses apply the 128-byte swizzle
+// (16-byte chunk c of row r lives at chunk c ^ (r & 7)), so the unpadded
+// 8 KB stage is bank-conflict free.
+__device__ __forceinline__ uint32_t sw128(uint32_t half_base, int r, int chunk) {
+    return half_base + r * 128 + ((chunk ^ (r & 7)) << 4);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kAttnThreads, 2) attention_tma_kernel(DevState s, AttnArgs a,
+                                                                         const __grid_constant__ CUtensorMap tmap) {
+    constexpr int HALVES = D / 64;       // 64-column boxes per page row
+    constexpr int PAGE_SM = 32 * 2 * D;  // HALVES x 4 KB (32 rows x 128 B each)
+    constexpr int NST = 3;
+    constexpr int KS = D / 16;
+    constexpr int NT = D / 8;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[kAttnThreads / 32][NST];
+    __shared__ int32_t ids[kAttnMaxSplitPages];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    const int i = blockIdx.y;
+    const int sp = blockIdx.x;
+    const int H = s.tab_heads;
+    const int h = i % H;
+    const int seq = i / H;
+    const int t = (seq * s.n_layers + a.layer) * H + h;
+    const int G = a.G;
+    const int N = s.num_pages[t];
+    const int p_begin = sp * a.pages_per_split;
+    const int p_end = min(N, p_begin + a.pages_per_split);
+    const int g = lane >> 2;
+    const int tq = lane & 3;
+    // SWIZZLE_128B destinations must be 1024-byte aligned: align the dynamic
+    // shared memory base by hand (the launch adds 1 KB of slack)
+    uint8_t* sbase = smem + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem)) & 1023u)) & 1023u);
+    uint8_t* stage = sbase + wid * NST * PAGE_SM;
+    float* wpart_o = reinterpret_cast<float*>(sbase + nw * NST * PAGE_SM);
+    float* wpart_ml = wpart_o + nw * G * D;
+    uint32_t qa[KS][2];
+    {
+        const uint8_t* qrow = a.q + ((int64_t)seq * a.n_q_heads + h * G + min(g, G - 1)) * (D * 2);
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            qa[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + (16 * ks + 2 * tq) * 2) : 0u;
+            qa[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + (16 * ks + 2 * tq + 8) * 2) : 0u;
+        }
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
+    const int my_n = (p_end - p_begin) > wid ? ((p_end - p_begin) - wid + nw - 1) / nw : 0;
+    const bool ids_sm = p_end - p_begin <= kAttnMaxSplitPages;
+    if (ids_sm)
+        for (int j = threadIdx.x; j < p_end - p_begin; j += blockDim.x) ids[j] = __ldg(row + p_begin + j);
+    if (lane < NST) {
+        const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[wid][lane]));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    auto issue = [&](int k) {
+        if (k < my_n && lane == 0) {
+            const int pg = p_begin + wid + k * nw;
+            const int32_t id = ids_sm ? ids[pg - p_begin] : __ldg(row + pg);
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(stage + (k % NST) * PAGE_SM));
+            const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[wid][k % NST]));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(PAGE_SM) : "memory");
+            const int y = id * 32;
+#pragma unroll
+            for (int hf = 0; hf < HALVES; ++hf)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                    ::"r"(dst + hf * 4096), "l"(&tmap), "r"(hf * 64), "r"(y), "r"(b)
+                    : "memory");
+        }
+    };
+    auto wait_stage = [&](int k) {
+        const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[wid][k % NST]));
+        const uint32_t parity = (k / NST) & 1;
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 %0, 1, 0, P1;\n\t}"
+                         : "=r"(done) : "r"(b), "r"(parity) : "memory");
+    };
+#pragma unroll
+    for (int k = 0; k < NST - 1; ++k) issue(k);
+    const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+    const int lm_j = lane >> 3, lm_r = lane & 7;
+    for (int k = 0; k < my_n; ++k) {
+        issue(k + NST - 1);
+        wait_stage(k);
+        const int pg = p_begin + wid + k * nw;
+        const int fill = (pg == N - 1) ? s.newest_fill[t] : 16;
+        const uint32_t st = stage_s + (k % NST) * PAGE_SM;
+        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            uint32_t b0, b1, b2, b3;
+            const int tok = (lm_j >> 1) * 8 + lm_r;
+            const int c = 2 * ks + (lm_j & 1);  // 16-byte chunk of d (8 elements)
+            ldsm_x4(sw128(st + (c >> 3) * 4096, tok, c & 7), b0, b1, b2, b3);
+            mma_bf16_16816(sc[0], qa[ks][0], qa[ks][1], b0, b1);
+            mma_bf16_16816(sc[1], qa[ks][0], qa[ks][1], b2, b3);
+        }
+        float x[2][2];
+        float rmax = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int tok = 8 * nt + 2 * tq + j;
+                x[nt][j] = tok < fill ? sc[nt][j] * a.scale_log2 : -INFINITY;
+                rmax = fmaxf(rmax, x[nt][j]);
+            }
+        }
+        rmax = fmaxf(rmax, __shfl_xor_sync(0xFFFFFFFFu, rmax, 1));
+        rmax = fmaxf(rmax, __shfl_xor_sync(0xFFFFFFFFu, rmax, 2));
+        const float m_new = fmaxf(m, rmax);
+        const float corr = exp2f(m - m_new);
+        float rsum = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                x[nt][j] = exp2f(x[nt][j] - m_new);
+                rsum += x[nt][j];
+            }
+        }
+        rsum += __shfl_xor_sync(0xFFFFFFFFu, rsum, 1);
+        rsum += __shfl_xor_sync(0xFFFFFFFFu, rsum, 2);
+        l = l * corr + rsum;
+        m = m_new;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            o[nt][0] *= corr;
+            o[nt][1] *= corr;
+        }
+        uint32_t ph0, pl0, ph1, pl1;
+        split_bf16x2(x[0][0], x[0][1], ph0, pl0);
+        split_bf16x2(x[1][0], x[1][1], ph1, pl1);
+#pragma unroll
+        for (int ntp = 0; ntp < NT / 2; ++ntp) {
+            uint32_t b0, b1, b2, b3;
+            const int tok = (lm_j & 1) * 8 + lm_r;
+            const int c = 2 * ntp + (lm_j >> 1);
+            ldsm_x4_t(sw128(st + (c >> 3) * 4096, 16 + tok, c & 7), b0, b1, b2, b3);
+            mma_bf16_16816(o[2 * ntp], ph0, ph1, b0, b1);
+            mma_bf16_16816(o[2 * ntp], pl0, pl1, b0, b1);
+            mma_bf16_16816(o[2 * ntp + 1], ph0, ph1, b2, b3);
+            mma_bf16_16816(o[2 * ntp + 1], pl0, pl1, b2, b3);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    if (g < G) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            wpart_o[(wid * G + g) * D + 8 * nt + 2 * tq] = o[nt][0];
+            wpart_o[(wid * G + g) * D + 8 * nt + 2 * tq + 1] = o[nt][1];
+        }
+        if (tq == 0) {
+            wpart_ml[(wid * G + g) * 2] = m;
+            wpart_ml[(wid * G + g) * 2 + 1] = l;
+        }
+    }
+    __syncthreads();
+    const int n_splits = a.splits;
+    for (int xi = threadIdx.x; xi < G * D; xi += blockDim.x) {
+        const int gg = xi / D;
+        float mm = -INFINITY;
+        for (int w2 = 0; w2 < nw; ++w2) mm = fmaxf(mm, wpart_ml[(w2 * G + gg) * 2]);
+        float ll = 0.f, oo = 0.f;
+        for (int w2 = 0; w2 < nw; ++w2) {
+            const float mw = wpart_ml[(w2 * G + gg) * 2];
+            const float c = (mw == -INFINITY) ? 0.f : exp2f(mw - mm);
+            ll += wpart_ml[(w2 * G + gg) * 2 + 1] * c;
+            oo += wpart_o[(w2 * G + gg) * D + (xi % D)] * c;
+        }
+        if (n_splits == 1) {
+            a.out[((int64_t)seq * a.n_q_heads + h * G + gg) * D + (xi % D)] = oo / ll;
+            continue;
+        }
+        const int64_t pidx = ((int64_t)i * n_splits + sp) * G + gg;
+        a.part_o[pidx * D + (xi % D)] = oo;
+        if (xi % D == 0) {
+            a.part_ml[pidx * 2] = mm;
+            a.part_ml[pidx * 2 + 1] = ll;
+        }
+    }
+    if (n_splits > 1) merge_if_last(s, a, i, D);
+}
+
+size_t attention_tma_smem(int d, int G) {
+    const int nw = kAttnThreads / 32;
+    return 1024 + (size_t)nw * 3 * 32 * 2 * d + (size_t)nw * G * d * 4 + (size_t)nw * G * 2 * 4;
+}
+
+void launch_attention_tma(int d, dim3 grid, size_t smem, cudaStream_t st, const DevState& s, const AttnArgs& a,
+                          const void* tmap) {
+    const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap);
+    if (d == 128) attention_tma_kernel<128><<<grid, kAttnThreads, smem, st>>>(s, a, tm);
+    else attention_tma_kernel<64><<<grid, kAttnThreads, smem, st>>>(s, a, tm);
+}
+
+const void* attention_tma_fn(int d) {
+    return d == 128 ? reinterpret_cast<const void*>(attention_tma_kernel<128>)
+                    : reinterpret_cast<const void*>(attention_tma_kernel<64>);
 }
 
 }  // namespace pe

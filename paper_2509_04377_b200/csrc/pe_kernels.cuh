@@ -70,6 +70,11 @@ __global__ void attention_split_kernel(DevState s, AttnArgs a);
 size_t attention_mma_smem(int d, int G);
 void launch_attention_mma(int d, dim3 grid, size_t smem, cudaStream_t st, const DevState& s, const AttnArgs& a);
 const void* attention_mma_fn(int d);
+// TMA (tensor map, SWIZZLE_128B) staging variant for d in {64, 128} (pe_attention.cu)
+size_t attention_tma_smem(int d, int G);
+void launch_attention_tma(int d, dim3 grid, size_t smem, cudaStream_t st, const DevState& s, const AttnArgs& a,
+                          const void* tmap);
+const void* attention_tma_fn(int d);
 
 // table-granular kernels (pe_table.cu)
 __global__ void pool_allocate_kernel(DevState s, int32_t* out);
