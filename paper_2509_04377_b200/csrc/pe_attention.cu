@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 
 #include "pe_kernels.cuh"
+#include "pe_tma.cuh"
 
 namespace pe {
 
@@ -535,10 +536,6 @@ const void* attention_mma_fn(int d) {
 // cp.async per page; ldmatrix addresses apply the 128-byte swizzle
 // (16-byte chunk c of row r lives at chunk c ^ (r & 7)), so the unpadded
 // 8 KB stage is bank-conflict free.
-__device__ __forceinline__ uint32_t sw128(uint32_t half_base, int r, int chunk) {
-    return half_base + r * 128 + ((chunk ^ (r & 7)) << 4);
-}
-
 template <int D>
 __global__ void __launch_bounds__(kAttnThreads, 2) attention_tma_kernel(DevState s, AttnArgs a,
                                                                          const __grid_constant__ CUtensorMap tmap) {
@@ -567,7 +564,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_tma_kernel(DevState
     const int tq = lane & 3;
     // SWIZZLE_128B destinations must be 1024-byte aligned: align the dynamic
     // shared memory base by hand (the launch adds 1 KB of slack)
-    uint8_t* sbase = smem + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem)) & 1023u)) & 1023u);
+    uint8_t* sbase = align1024(smem);
     uint8_t* stage = sbase + wid * NST * PAGE_SM;
     float* wpart_o = reinterpret_cast<float*>(sbase + nw * NST * PAGE_SM);
     float* wpart_ml = wpart_o + nw * G * D;
@@ -589,37 +586,18 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_tma_kernel(DevState
     const bool ids_sm = p_end - p_begin <= kAttnMaxSplitPages;
     if (ids_sm)
         for (int j = threadIdx.x; j < p_end - p_begin; j += blockDim.x) ids[j] = __ldg(row + p_begin + j);
-    if (lane < NST) {
-        const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[wid][lane]));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (lane < NST) mbar_init(&bars[wid][lane], 1);
+    mbar_init_fence();
     __syncthreads();
     auto issue = [&](int k) {
         if (k < my_n && lane == 0) {
             const int pg = p_begin + wid + k * nw;
             const int32_t id = ids_sm ? ids[pg - p_begin] : __ldg(row + pg);
-            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(stage + (k % NST) * PAGE_SM));
-            const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[wid][k % NST]));
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(PAGE_SM) : "memory");
-            const int y = id * 32;
-#pragma unroll
-            for (int hf = 0; hf < HALVES; ++hf)
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                    ::"r"(dst + hf * 4096), "l"(&tmap), "r"(hf * 64), "r"(y), "r"(b)
-                    : "memory");
+            tma_load_page(smem_u32(stage + (k % NST) * PAGE_SM), &bars[wid][k % NST], &tmap, id * 32, HALVES,
+                          PAGE_SM);
         }
     };
-    auto wait_stage = [&](int k) {
-        const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[wid][k % NST]));
-        const uint32_t parity = (k / NST) & 1;
-        uint32_t done = 0;
-        while (!done)
-            asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 %0, 1, 0, P1;\n\t}"
-                         : "=r"(done) : "r"(b), "r"(parity) : "memory");
-    };
+    auto wait_stage = [&](int k) { mbar_wait(&bars[wid][k % NST], (k / NST) & 1); };
 #pragma unroll
     for (int k = 0; k < NST - 1; ++k) issue(k);
     const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));

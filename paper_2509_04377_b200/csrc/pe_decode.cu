@@ -286,6 +286,51 @@ __device__ __forceinline__ void push_victims_if_last(const DevState& s, int n, i
     if (threadIdx.x == 0) *s.top = top + base;
 }
 
+// Page mean of a 16-slot page from the lane-pair scores S (pair r = slot r),
+// in slot order (score_pages -> page_score, importance.cpp:19-30); with holes,
+// the mean over the occupied slots. Valid on every lane.
+template <bool HOLES>
+__device__ __forceinline__ double page_mean_b16(const DevState& s, int id, double S) {
+    double sum = 0.0;
+    if constexpr (!HOLES) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+        return sum / 16.0;
+    } else {
+        const unsigned long long hm = s.holes[id];
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const double x = __shfl_sync(0xFFFFFFFFu, S, 2 * j);
+            const bool occ = !((hm >> j) & 1ull);
+            sum += occ ? x : 0.0;  // S >= +0: adding +0 leaves the sum unchanged
+            cnt += occ;
+        }
+        return sum / static_cast<double>(cnt);
+    }
+}
+
+// End of a K2 chunk: publish this CTA's page means, take the table's ticket;
+// the table's last CTA takes the argmin and evicts. Returns the tables settled.
+__device__ __forceinline__ int publish_chunk(const DevState& s, int t, int y, int N, int p0, int np, int n_cta,
+                                             const double* page_mean, double* scratch, int32_t* tickets,
+                                             int32_t* vpage, int32_t* victims) {
+    __shared__ int last;
+    __syncthreads();
+    for (int j = threadIdx.x; j < np; j += blockDim.x) scratch[(int64_t)y * s.max_pages + p0 + j] = page_mean[j];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(&tickets[y], 1) == n_cta - 1);
+    __syncthreads();
+    if (!last) return 0;
+    __threadfence();
+    if ((threadIdx.x >> 5) == 0) {
+        finalize_evict(s, t, y, N, scratch + (int64_t)y * s.max_pages, vpage, victims);
+        if ((threadIdx.x & 31) == 0) tickets[y] = 0;
+    }
+    return 1;
+}
+
 // ---------------------------------------------------------------------------
 // evict_score_kernel (K2, recompute): grid (launch tables, chunks). CTA (y, c)
 // scores pages [c*P, c*P+P) of table y if it triggers; each warp takes whole
@@ -299,7 +344,6 @@ __global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
     DevState s, TableSet ts, int pages_per_cta, double* scratch, int32_t* tickets, int32_t* vpage,
     int32_t* victims, unsigned long long grid_last) {
     __shared__ double page_mean[kMaxPagesPerCta];
-    __shared__ int last;
     const int y = blockIdx.x;
     const int c = blockIdx.y;
     const int t = ts.table(s, y);
@@ -332,23 +376,8 @@ __global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
                 const int id = __ldg(row + p0 + lp);
                 const uint8_t* base = s.pages + (int64_t)id * page_bytes;
                 const double S = pair_token_score<SV>(base + ko, base + vo, true, s.w, s.dtype);
-                double sum = 0.0;
-                if constexpr (!HOLES) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * j);
-                    if (lane == 0) page_mean[lp] = sum / 16.0;
-                } else {  // mean over the occupied slots (page_score, importance.cpp:19-30)
-                    const unsigned long long hm = s.holes[id];
-                    int cnt = 0;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const double x = __shfl_sync(0xFFFFFFFFu, S, 2 * j);
-                        const bool occ = !((hm >> j) & 1ull);
-                        sum += occ ? x : 0.0;  // S >= +0: adding +0 leaves the sum unchanged
-                        cnt += occ;
-                    }
-                    if (lane == 0) page_mean[lp] = sum / static_cast<double>(cnt);
-                }
+                const double mean = page_mean_b16<HOLES>(s, id, S);
+                if (lane == 0) page_mean[lp] = mean;
             }
         } else {
             for (int lp = wid; lp < np; lp += nw) {
@@ -374,20 +403,7 @@ __global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
                 if (lane == 0) page_mean[lp] = sum / static_cast<double>(cnt);
             }
         }
-        __syncthreads();
-        for (int j = threadIdx.x; j < np; j += blockDim.x) scratch[(int64_t)y * s.max_pages + p0 + j] = page_mean[j];
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) last = (atomicAdd(&tickets[y], 1) == n_cta - 1);
-        __syncthreads();
-        if (last) {
-            __threadfence();
-            if (wid == 0) {
-                finalize_evict(s, t, y, N, scratch + (int64_t)y * s.max_pages, vpage, victims);
-                if (lane == 0) tickets[y] = 0;
-            }
-            settled = 1;
-        }
+        settled = publish_chunk(s, t, y, N, p0, np, n_cta, page_mean, scratch, tickets, vpage, victims);
     }
     push_victims_if_last(s, ts.size(s), vpage, grid_last, settled);
 }
