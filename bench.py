@@ -318,13 +318,20 @@ def run_b200(args, cfg, world, rank, local):
 
     cycles = [0]  # eviction cycles run on every table (cadence check)
 
+    k0_evs = []  # (start, end) around each cycle's B append launches (timed cycles only)
+
     def cycle(record=None, host=False, mode=pe.ScoreMode.RECOMPUTE, victims_host=None):
         cycles[0] += 1
+        if record is not None and not host and mode == pe.ScoreMode.RECOMPUTE:
+            k0_evs.append((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)))
+            k0_evs[-1][0].record(stream)
         for j in range(B):
             if host:
                 eng.append_token(0, NL, h_k[j], h_v[j], next_pos())
             else:
                 eng.append_token(0, NL, rows_k[j], rows_v[j], next_pos())
+        if record is not None and not host and mode == pe.ScoreMode.RECOMPUTE:
+            k0_evs[-1][1].record(stream)
         spans = [(0, NL)] if args.evict_launch == "step" else [(layer, 1) for layer in range(NL)]
         for l0, nl in spans:
             vh = victims_host[: nl * n_tab_layer] if victims_host is not None else None
@@ -497,6 +504,7 @@ def run_b200(args, cfg, world, rank, local):
             "pct_of_peak": round(100 * value / world / peak, 2),
             "p50_evict_step_us": round(statistics.median(k2_ms) * 1e3, 2),
             "p50_evict_step_us_cached": round(k2c_us, 2),
+            "append_us_per_launch_p50": round(statistics.median(a.elapsed_time(b) for a, b in k0_evs) * 1e3 / B, 2),
             "evict_launch": args.evict_launch,
             f"p50_evict_{other}_launch_us": round(other_us, 2),
             f"evict_{other}_launch_gbs": round(other_bytes / (other_us * 1e-6) / 1e9, 1),

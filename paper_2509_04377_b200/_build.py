@@ -24,7 +24,7 @@ FACADE_SRC = PKG / "cpp" / "pagedevict.cpp"
 FACADE_HDR = ROOT / "include" / "pe" / "pagedevict.hpp"
 FACADE_LIB = LIB_DIR / "libpagedevict_b200.so"
 SOURCES = ["pe_engine.cu", "pe_decode.cu", "pe_prefill.cu", "pe_attention.cu", "pe_table.cu"]
-HEADERS = ["pe_internal.cuh", "pe_kernels.cuh", "pe_score.cuh"]
+HEADERS = ["pe_internal.cuh", "pe_kernels.cuh", "pe_score.cuh", "pe_tma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -73,6 +73,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
         f"-I{ROOT / 'include'}", f"-I{CSRC}",
+        *os.environ.get("PE_NVCC_EXTRA", "").split(),  # e.g. -DPE_K0_TRACE for instrumented A/B builds
         *[str(CSRC / s) for s in SOURCES],
         "-o", str(tmp),
     ]

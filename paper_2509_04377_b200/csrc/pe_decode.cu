@@ -6,6 +6,10 @@
 #include "pe_kernels.cuh"
 #include "pe_score.cuh"
 
+#ifdef PE_K0_TRACE
+#include <cstdio>
+#endif
+
 namespace pe {
 
 // ---------------------------------------------------------------------------
@@ -21,23 +25,17 @@ namespace pe {
 // (PoolExhausted, page_pool.cpp:26-28) and no later table of the launch is
 // appended (the exception would have stopped the loop).
 constexpr unsigned long long kLbAgg = 1ull << 30;
-constexpr unsigned long long kLbInc = 2ull << 30;
 
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+// Every look-back word is self-contained (epoch, flag and value in one 64-bit
+// word, nothing else published through it), so relaxed gpu-scope accesses
+// suffice: no release fences (MEMBAR.GPU) on the critical path.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire_i32(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_i32(int* p, int v) {
-    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -53,9 +51,18 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
                                                                  const uint8_t* __restrict__ k_rows,
                                                                  const uint8_t* __restrict__ v_rows,
                                                                  const int64_t* __restrict__ positions,
-                                                                 unsigned long long* lb_status, LaunchCtl* ctl,
+                                                                 unsigned long long* lb_status,
+                                                                 unsigned long long* lb_group, LaunchCtl* ctl,
                                                                  unsigned long long ticket_base, int epoch) {
     __shared__ int sh_lid, sh_warp_cnt[kAppendThreads / 32], sh_prefix, sh_pop_base;
+#ifdef PE_K0_TRACE
+    unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int polls = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr[0]));
+#define PE_TR(i) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr[i]))
+#else
+#define PE_TR(i)
+#endif
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = kAppendThreads / 32;
@@ -63,6 +70,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
     const int n_ctas = (n + 16 * nw - 1) / (16 * nw);
     if (threadIdx.x == 0) sh_lid = static_cast<int>(atomicAdd(s.grid_ctr, 1ull) - ticket_base);
     __syncthreads();
+    PE_TR(1);
     const int lid = sh_lid;
     const int i0 = (lid * nw + wid) * 16;
     const int my_i = i0 + (lane >> 1);
@@ -86,45 +94,65 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
     const unsigned pop_mask = __ballot_sync(0xFFFFFFFFu, pop && q == 0);
     if (lane == 0) sh_warp_cnt[wid] = __popc(pop_mask);
     __syncthreads();
+    PE_TR(2);
     if (wid == 0) {
         int local = 0;
         for (int w = 0; w < nw; ++w) local += sh_warp_cnt[w];
         const unsigned long long ep = static_cast<unsigned long long>(static_cast<unsigned>(epoch)) << 32;
-        int prefix = 0;
-        if (lid == 0) {
-            if (lane == 0) {
-                const int top = *s.top;
-                ctl->pop_base = top;
-                st_release_u64(lb_status, ep | kLbInc | static_cast<unsigned long long>(local));
-                st_release_i32(&ctl->ready, epoch);
-                sh_pop_base = top;
+        // Two-level look-back: CTA lid = 32g + r publishes its pop count; it
+        // sums the counts of CTAs 32g .. lid-1 (lane l reads CTA 32g + l) and
+        // the aggregates of groups 0 .. g-1, which the last CTA of each group
+        // publishes after its own in-group sum. Every word waited on belongs
+        // to a lower lid (deadlock-free in arrival order) and a CTA issues at
+        // most 31 + ceil(g/32)*32 loads: all-pairs windows (O(n^2) loads on a
+        // few status lines) congested their L2 slices for ~10 us.
+        const int g = lid >> 5, r = lid & 31;
+        if (lane == 0) {
+            st_relaxed_u64(lb_status + lid, ep | kLbAgg | static_cast<unsigned long long>(local));
+            if (lid == 0) {
+                const int top0 = *s.top;
+                st_relaxed_u64(&ctl->top_word, ep | static_cast<unsigned>(top0));
+                sh_pop_base = top0;
             }
-        } else {
-            if (lane == 0) st_release_u64(lb_status + lid, ep | kLbAgg | static_cast<unsigned long long>(local));
-            // warp-parallel look-back: lane l reads predecessor j - l; the window
-            // ends at the closest predecessor that has published its inclusive
-            // prefix (CTA 0 always has)
-            for (int j = lid - 1;; j -= 32) {
-                const int idx = j - lane;
-                unsigned long long w = 0;
-                if (idx >= 0) {
-                    do {
-                        w = ld_acquire_u64(lb_status + idx);
-                    } while ((w >> 32) != static_cast<unsigned>(epoch));  // not yet published
-                }
-                const unsigned inc_mask = __ballot_sync(0xFFFFFFFFu, idx >= 0 && (w & kLbInc));
-                const int stop = inc_mask ? __ffs(inc_mask) - 1 : 31;
-                int v = (idx >= 0 && lane <= stop) ? static_cast<int>(w & ((1ull << 30) - 1)) : 0;
+        }
+        // the stack top CTA 0 publishes: first read issued now, re-polled below
+        unsigned long long tw = (lane == 0 && lid != 0) ? ld_relaxed_u64(&ctl->top_word) : 0ull;
+        unsigned long long w = 0;
+        if (lane < r) {
+            w = ld_relaxed_u64(lb_status + 32 * g + lane);
+            while ((w >> 32) != static_cast<unsigned>(epoch)) {  // not yet published
+                __nanosleep(64);
+                w = ld_relaxed_u64(lb_status + 32 * g + lane);
+            }
+        }
+        int in_grp = lane < r ? static_cast<int>(w & ((1ull << 30) - 1)) : 0;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-                prefix += v;
-                if (inc_mask) break;
+        for (int o = 16; o > 0; o >>= 1) in_grp += __shfl_xor_sync(0xFFFFFFFFu, in_grp, o);
+        if (lane == 0 && (r == 31 || lid == n_ctas - 1))
+            st_relaxed_u64(lb_group + g, ep | static_cast<unsigned long long>(in_grp + local));
+        int prefix = in_grp;
+        for (int g0 = 0; g0 < g; g0 += 32) {
+            unsigned long long gw = 0;
+            if (g0 + lane < g) {
+                gw = ld_relaxed_u64(lb_group + g0 + lane);
+                while ((gw >> 32) != static_cast<unsigned>(epoch)) {
+                    __nanosleep(64);
+                    gw = ld_relaxed_u64(lb_group + g0 + lane);
+                }
             }
-            if (lane == 0) {
-                st_release_u64(lb_status + lid, ep | kLbInc | static_cast<unsigned long long>(prefix + local));
-                while (ld_acquire_i32(&ctl->ready) != epoch) __nanosleep(32);
-                sh_pop_base = ctl->pop_base;
+            int v = g0 + lane < g ? static_cast<int>(gw & ((1ull << 30) - 1)) : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+            prefix += v;
+        }
+        PE_TR(6);
+        if (lane == 0 && lid != 0) {
+            while ((tw >> 32) != static_cast<unsigned>(epoch)) {
+                __nanosleep(64);
+                tw = ld_relaxed_u64(&ctl->top_word);
             }
+            sh_pop_base = static_cast<int>(tw & 0xFFFFFFFFull);
+            PE_TR(7);
         }
         if (lane == 0) {
             if (lid == n_ctas - 1) {
@@ -135,6 +163,8 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
         }
     }
     __syncthreads();
+    PE_TR(3);
+
     // rank of this table's pop among the launch's pops (ascending table id);
     // for a non-popping table: the number of pops before it
     int rank = sh_prefix;
@@ -158,13 +188,18 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
         s.block_table[(int64_t)t * s.max_pages + np] = page;
         s.num_pages[t] = np + 1;
     }
-    const int64_t in_row = served ? ts.input_row(s, my_i) : 0;
-    const uint8_t* krow = k_rows + in_row * s.row_bytes;
-    const uint8_t* vrow = v_rows + in_row * s.row_bytes;
     uint8_t* kdst = s.pages + (((int64_t)page * 2 + 0) * s.B + slot) * s.pitch;
     uint8_t* vdst = s.pages + (((int64_t)page * 2 + 1) * s.B + slot) * s.pitch;
-    const double S = pair_token_score<SV>(krow, vrow, served, s.w, s.dtype, served ? kdst : nullptr,
-                                          served ? vdst : nullptr);
+    PE_TR(4);
+    const int64_t in_row = served ? ts.input_row(s, my_i) : 0;
+    const double S = pair_token_score<SV>(k_rows + in_row * s.row_bytes, v_rows + in_row * s.row_bytes, served, s.w,
+                                          s.dtype, served ? kdst : nullptr, served ? vdst : nullptr);
+    PE_TR(5);
+#ifdef PE_K0_TRACE
+    if (threadIdx.x == 0 && epoch % 64 == 40)
+        printf("K0TRACE epoch %d lid %d t0 %llu t1 %llu t2 %llu walk %llu top %llu t3 %llu t4 %llu t5 %llu\n", epoch, lid,
+               tr[0], tr[1], tr[2], tr[6], tr[7], tr[3], tr[4], tr[5]);
+#endif
     if (served && q == 0) {
         const int64_t ps = (int64_t)page * s.B + slot;
         s.positions[ps] = static_cast<int32_t>(positions[ts.pos_index(s, my_i)]);
@@ -175,10 +210,20 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
             // page_score, importance.cpp:19-30: mean over the occupied slots in slot order
             double sum = 0.0;
             int cnt = 1;
-            for (int j = 0; j < s.B - 1; ++j) {
-                if (slot_hole(s, page, j)) continue;
-                sum += s.token_scores[(int64_t)page * s.B + j];
-                ++cnt;
+            const double* ts_page = s.token_scores + (int64_t)page * s.B;
+            if (s.B == 16 && !s.holes_on) {  // independent loads, then the slot-order sum
+                double x[15];
+#pragma unroll
+                for (int j = 0; j < 15; ++j) x[j] = ts_page[j];
+#pragma unroll
+                for (int j = 0; j < 15; ++j) sum += x[j];
+                cnt = 16;
+            } else {
+                for (int j = 0; j < s.B - 1; ++j) {
+                    if (slot_hole(s, page, j)) continue;
+                    sum += ts_page[j];
+                    ++cnt;
+                }
             }
             sum += S;
             s.page_scores[page] = sum / static_cast<double>(cnt);
@@ -421,9 +466,10 @@ void launch_evict_score(dim3 grid, int threads, cudaStream_t st, const DevState&
 
 template <int SV>
 void launch_append(int blocks, cudaStream_t st, const DevState& s, const TableSet& ts, const uint8_t* k,
-                   const uint8_t* v, const int64_t* pos, unsigned long long* lb, LaunchCtl* ctl,
+                   const uint8_t* v, const int64_t* pos, unsigned long long* lb, unsigned long long* lbg,
+                   LaunchCtl* ctl,
                    unsigned long long ticket_base, int epoch) {
-    append_kernel<SV><<<blocks, kAppendThreads, 0, st>>>(s, ts, k, v, pos, lb, ctl, ticket_base, epoch);
+    append_kernel<SV><<<blocks, kAppendThreads, 0, st>>>(s, ts, k, v, pos, lb, lbg, ctl, ticket_base, epoch);
 }
 
 void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st, const DevState& s,
@@ -435,8 +481,9 @@ void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st
 
 void launch_append_any(int variant, int blocks, cudaStream_t st, const DevState& s, const TableSet& ts,
                        const uint8_t* k, const uint8_t* v, const int64_t* pos, unsigned long long* lb,
+                       unsigned long long* lbg,
                        LaunchCtl* ctl, unsigned long long ticket_base, int epoch) {
-    PE_SCORE_DISPATCH(variant, (launch_append<SV>(blocks, st, s, ts, k, v, pos, lb, ctl, ticket_base, epoch)));
+    PE_SCORE_DISPATCH(variant, (launch_append<SV>(blocks, st, s, ts, k, v, pos, lb, lbg, ctl, ticket_base, epoch)));
 }
 
 // ---------------------------------------------------------------------------

@@ -18,6 +18,11 @@ using namespace pe;
 
 namespace {
 
+// append look-back words: one per K0 CTA (64 tables each), then one per
+// group of 32 CTAs
+size_t lb_cta_words(int64_t n_tables) { return (size_t)n_tables / 64 + 2; }
+size_t lb_words(int64_t n_tables) { return lb_cta_words(n_tables) + lb_cta_words(n_tables) / 32 + 2; }
+
 thread_local std::string g_err;
 
 pe_status fail(pe_status s, const std::string& msg) {
@@ -324,7 +329,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         dalloc(&e->attn_tickets, n_tables) != cudaSuccess ||
         dalloc(&e->seq_units, c.n_seqs) != cudaSuccess || dalloc(&e->seq_done, c.n_seqs) != cudaSuccess ||
         dalloc(&e->work_ctr, 1) != cudaSuccess ||
-        dalloc(&e->lb_status, (size_t)n_tables / 64 + 2) != cudaSuccess ||
+        dalloc(&e->lb_status, lb_words(n_tables)) != cudaSuccess ||
         dalloc(&e->rank, n_tables) != cudaSuccess || dalloc(&e->work, n_tables) != cudaSuccess ||
         dalloc(&e->victims, n_tables) != cudaSuccess || dalloc(&e->tickets, n_tables) != cudaSuccess ||
         dalloc(&e->evict_scratch, (size_t)n_tables * max_pages) != cudaSuccess ||
@@ -361,7 +366,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             cudaMemset(s.grid_ctr, 0, sizeof(unsigned long long)) != cudaSuccess ||
             cudaMemset(e->tickets, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
             cudaMemset(e->attn_tickets, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
-            cudaMemset(e->lb_status, 0, sizeof(unsigned long long) * ((size_t)n_tables / 64 + 2)) != cudaSuccess ||
+            cudaMemset(e->lb_status, 0, sizeof(unsigned long long) * lb_words(n_tables)) != cudaSuccess ||
             cudaMemset(e->ctl, 0, sizeof(LaunchCtl)) != cudaSuccess ||
             cudaMemset(s.positions, 0xFF, sizeof(int32_t) * (size_t)cap * s.B) != cudaSuccess ||
             cudaMemset(s.holes, 0, sizeof(unsigned long long) * (size_t)cap) != cudaSuccess ||
@@ -731,7 +736,8 @@ pe_status launch_append(pe_engine* e, const TableSet& ts, const uint8_t* dk, con
     const unsigned long long ticket_base = e->grid_tickets;
     e->grid_tickets += blocks;
     e->append_epoch = (e->append_epoch % 0x3FFFFFFF) + 1;
-    launch_append_any(e->variant, blocks, st, s, ts, dk, dv, dp, e->lb_status, e->ctl, ticket_base, e->append_epoch);
+    launch_append_any(e->variant, blocks, st, s, ts, dk, dv, dp, e->lb_status,
+                      e->lb_status + lb_cta_words(s.n_tables), e->ctl, ticket_base, e->append_epoch);
     mark_consumed(e, st);
     pe_status r = check_launch(e, "append_kernel");
     if (r != PE_OK) return r;

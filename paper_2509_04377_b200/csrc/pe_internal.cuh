@@ -59,8 +59,9 @@ struct LaunchCtl {
     int32_t pop_base;   // stack top before this launch's pops
     int32_t push_base;  // stack top before this launch's pushes
     int32_t count;      // number of flagged tables (evict work items)
-    int32_t ready;      // epoch of the launch whose fields are valid (append look-back)
+    int32_t ready;      // unused (kept for layout)
     int32_t pad_;
+    unsigned long long top_word;  // append look-back: epoch << 32 | stack top before the launch's pops
 };
 
 // Launch table set: decode launches cover every sequence for layers
