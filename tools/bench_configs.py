@@ -117,6 +117,18 @@ def run(name, layers, kvh, d, qh, lens, C, dtype, decode_steps, waves=1, pool_la
     t1.record(st)
     t1.synchronize()
     dec_ms = t0.elapsed_time(t1)
+    # all-layer eviction launches (one per decode step, as bench.py): B more steps
+    all_ms = []
+    for j in range(B):
+        eng.append_token(0, layers, rk[j], rv[j], pos)
+        pos.add_(1)
+        a, b = ev(), ev()
+        a.record(st)
+        eng.evict(0, layers, step=decode_steps + j + 1, mode=pe.ScoreMode.RECOMPUTE)
+        b.record(st)
+        all_ms.append((a, b))
+    torch.cuda.synchronize()
+    all_ms = [a.elapsed_time(b) for a, b in all_ms]
     evicted = eng.stats().pages_evicted - evicted0
     # eviction launches at a trigger step (all tables of the layer triggered together in uniform configs)
     trig = [a.elapsed_time(b) for a, b in k2_ms]
@@ -145,6 +157,12 @@ def run(name, layers, kvh, d, qh, lens, C, dtype, decode_steps, waves=1, pool_la
         p50 = statistics.median(trig)
         line["evict_step_gbs"] = round(k2_bytes / (p50 * 1e-3) / 1e9, 1)
         line["evict_step_frac"] = round(line["evict_step_gbs"] / PEAK, 4)
+        # one launch for all layers at the trigger step (the last of the B steps)
+        line["evict_all_layers_us"] = round(all_ms[-1] * 1e3, 2)
+        line["evict_all_layers_gbs"] = round(layers * k2_bytes / (all_ms[-1] * 1e-3) / 1e9, 1)
+        line["evict_all_layers_frac"] = round(line["evict_all_layers_gbs"] / PEAK, 4)
+    else:
+        line["evict_all_layers_us_mean"] = round(statistics.mean(all_ms) * 1e3, 2)
     print(json.dumps(line), flush=True)
     del eng
     torch.cuda.empty_cache()
