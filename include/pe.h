@@ -172,6 +172,29 @@ pe_status pe_decode_step(pe_engine* eng, int32_t layer_begin, int32_t n_layers,
 pe_status pe_paged_decode_attention(pe_engine* eng, int32_t layer, const void* q, float* out,
                                     int32_t n_q_heads, void* stream);
 
+/* Step-log capture (StepRecord, metrics.hpp:18-28; schemas/steplog.jsonl.md):
+ * the engine-owned fields of one decode step per table. retained_len and
+ * page_count as BlockTable::retained_len / page_count, newest_fill = occupied
+ * slots of the newest page (Page::fill), victim = the evicted logical page
+ * or -1 (EvictionDecision::Page / None). fragmentation and
+ * fragmentation_excl_newest follow from these exactly as in
+ * block_table.cpp:48-63 (pagedevict::step_records in the C++ façade,
+ * paper_2509_04377_b200.steplog in Python). */
+typedef struct pe_step_entry {
+    int32_t retained_len;
+    int32_t page_count;
+    int32_t newest_fill;
+    int32_t victim;
+} pe_step_entry;
+
+/* Writes one pe_step_entry per table of layers [layer_begin,
+ * layer_begin+n_layers) in launch order into out (host or device,
+ * stream-ordered). victims: the array (device) given to the preceding
+ * pe_decode_evict / pe_decode_step over the same tables, or NULL for that
+ * call's engine-side copy (when it was given a host array or none). */
+pe_status pe_step_log_capture(pe_engine* eng, int32_t layer_begin, int32_t n_layers, const int32_t* victims,
+                              pe_step_entry* out, void* stream);
+
 /* Synchronises the engine's device work and returns the device status word
  * (PE_OK or the first failure since the last pe_sync). */
 pe_status pe_sync(pe_engine* eng);

@@ -370,6 +370,71 @@ std::vector<float> attend(const AttentionInputs& inputs);
 AttentionDetail attend_detailed(const AttentionInputs& inputs);
 double output_deviation(std::span<const float> a, std::span<const float> b);
 
+// ------------------------------------------------------------------ metrics
+// metrics.hpp:16-80 and schemas/{steplog.jsonl,metrics.csv}.md: the per-step
+// log record, the per-run CSV record, their emitters and the per-policy
+// summary. Byte-identical output to the reference for the same records
+// (tests/cpp/scenario_trace.cpp runs both builds). Device-side capture of
+// the engine-owned StepRecord fields: pe_step_log_capture (pe.h) and
+// step_records() below.
+struct StepRecord {
+    std::uint32_t run = 0;
+    std::uint32_t sequence = 0;
+    std::uint32_t layer = 0;
+    std::int64_t step = 0;  // 1-based
+    std::size_t retained_len = 0;
+    EvictionDecision decision;
+    double fragmentation = 0.0;
+    double fragmentation_excl_newest = 0.0;
+    double deviation = 0.0;  // NaN: no FullCache shadow
+};
+
+struct MetricsRecord {
+    std::string policy;
+    std::uint64_t cache_budget = 0;
+    std::uint32_t page_size = 0;
+    std::uint64_t prefill_len = 0;
+    std::uint64_t decode_steps = 0;
+    std::uint64_t batch = 0;
+    std::uint64_t layer_count = 0;
+    std::uint64_t seed = 0;
+    std::uint64_t prefill_evicted = 0;
+    std::uint64_t evictions_total = 0;
+    std::uint64_t page_evictions = 0;
+    std::uint64_t token_evictions = 0;
+    std::uint64_t block_table_updates = 0;
+    double mean_fragmentation = 0.0;
+    double max_fragmentation = 0.0;
+    double max_fragmentation_excl_newest = 0.0;
+    double mean_deviation = 0.0;
+    double p95_deviation = 0.0;
+    std::uint64_t retained_bytes = 0;
+    std::uint64_t prefill_wall_ns = 0;
+    std::uint64_t decode_wall_ns = 0;
+};
+
+std::string emit_csv(std::span<const MetricsRecord> records);
+std::string emit_jsonl(std::span<const StepRecord> steps);
+
+struct SummaryRow {
+    std::string policy;
+    std::uint64_t runs = 0;
+    std::uint64_t evictions_total = 0;
+    std::uint64_t block_table_updates = 0;
+    double cadence_ratio = 0.0;  // NaN without a PagedEviction record
+    double max_fragmentation_excl_newest = 0.0;
+    double mean_deviation = 0.0;
+};
+
+std::vector<SummaryRow> summarize(std::span<const MetricsRecord> records);
+std::string format_summary(std::span<const SummaryRow> rows);
+
+// StepRecords (decision, retained length, both fragmentation ratios) for the
+// tables of one pe_step_log_capture, in the capture's table order; page
+// decisions carry trigger_step = step. `page_size` is the engine's B.
+std::vector<StepRecord> step_records(std::span<const pe_step_entry> entries, std::uint32_t page_size,
+                                     std::int64_t step, std::uint32_t run = 0);
+
 }  // namespace pagedevict
 
 // Integration self-test (one PagedEviction table on the device, invariants

@@ -312,6 +312,8 @@ class Reference:
         lib.ref_page_count.argtypes = [C.c_void_p, C.c_size_t]
         lib.ref_retained_len.restype = C.c_size_t
         lib.ref_retained_len.argtypes = [C.c_void_p, C.c_size_t]
+        lib.ref_fragmentation.restype = None
+        lib.ref_fragmentation.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p]
         lib.ref_free_count.restype = C.c_size_t
         lib.ref_free_count.argtypes = [C.c_void_p]
         lib.ref_read_table.argtypes = [C.c_void_p, C.c_size_t] + [C.c_void_p] * 5
@@ -460,6 +462,12 @@ class RefSession:
 
     def retained_len(self, t) -> int:
         return self.lib.ref_retained_len(self.h, t)
+
+    def fragmentation(self, t) -> tuple[float, float]:
+        """(fragmentation_ratio, fragmentation_ratio_excluding_newest)."""
+        out = (C.c_double * 2)()
+        self.lib.ref_fragmentation(self.h, t, out)
+        return out[0], out[1]
 
     def free_count(self) -> int:
         return self.lib.ref_free_count(self.h)

@@ -342,6 +342,12 @@ std::size_t ref_retained_len(void* h, std::size_t t) {
     return static_cast<Session*>(h)->tables.at(t).retained_len();
 }
 std::size_t ref_free_count(void* h) { return static_cast<Session*>(h)->pool.free_count(); }
+// BlockTable::fragmentation_ratio / _excluding_newest (step-log fields)
+void ref_fragmentation(void* h, std::size_t t, double* out2) {
+    const auto& table = static_cast<Session*>(h)->tables.at(t);
+    out2[0] = table.fragmentation_ratio();
+    out2[1] = table.fragmentation_ratio_excluding_newest();
+}
 
 // Logical-order readback of one table: physical ids [page_count], per page
 // fill [page_count], and per retained token (logical order, holes skipped)

@@ -13,6 +13,10 @@
 #include "pe/pagedevict.hpp"
 
 #include <algorithm>
+#include <array>
+#include <charconv>
+#include <cmath>
+#include <map>
 #include <cstdio>
 #include <cstring>
 #include <limits>
@@ -923,6 +927,190 @@ double output_deviation(std::span<const float> a, std::span<const float> b) {
         ref += static_cast<double>(b[i]) * static_cast<double>(b[i]);
     }
     return std::sqrt(diff) / std::max(std::sqrt(ref), 1e-12);
+}
+
+// ------------------------------------------------------------------ metrics
+// metrics.cpp's emitters restated: CSV numbers in the shortest round-trip
+// form (std::to_chars), JSON in the layout of the reference's JSON library
+// (compact, fixed field order, doubles as shortest digits with a ".0" on
+// integral values and an exponent outside 1e-5 .. 1e15, NaN as null).
+namespace {
+
+std::string csv_double(double v) {
+    std::array<char, 64> buf;
+    const auto res = std::to_chars(buf.data(), buf.data() + buf.size(), v);
+    return std::string(buf.data(), res.ptr);
+}
+
+std::string csv_field(const std::string& f) {
+    if (f.find_first_of(",\"\n") == std::string::npos) return f;
+    std::string q = "\"";
+    for (const char c : f) {
+        if (c == '"') q += '"';
+        q += c;
+    }
+    return q + "\"";
+}
+
+std::string json_double(double v) {
+    if (!std::isfinite(v)) return "null";
+    if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
+    std::array<char, 64> buf;
+    const auto res = std::to_chars(buf.data(), buf.data() + buf.size(), v, std::chars_format::scientific);
+    const std::string sci(buf.data(), res.ptr);  // [-]d[.ddd]e(+|-)XX
+    std::string out = sci[0] == '-' ? "-" : "";
+    const std::size_t m0 = out.size();
+    const std::size_t epos = sci.find('e');
+    std::string digits;
+    for (std::size_t i = m0; i < epos; ++i)
+        if (sci[i] != '.') digits += sci[i];
+    const int k = static_cast<int>(digits.size());
+    const int n = std::stoi(sci.substr(epos + 1)) + 1;  // decimal point after n digits
+    if (k <= n && n <= 15) {
+        out += digits + std::string(static_cast<std::size_t>(n - k), '0') + ".0";
+    } else if (0 < n && n <= 15) {
+        out += digits.substr(0, static_cast<std::size_t>(n)) + "." + digits.substr(static_cast<std::size_t>(n));
+    } else if (-4 < n && n <= 0) {
+        out += "0." + std::string(static_cast<std::size_t>(-n), '0') + digits;
+    } else {
+        out += digits.substr(0, 1);
+        if (k > 1) out += "." + digits.substr(1);
+        const int e = n - 1;
+        char eb[16];
+        std::snprintf(eb, sizeof eb, "e%c%02d", e < 0 ? '-' : '+', e < 0 ? -e : e);
+        out += eb;
+    }
+    return out;
+}
+
+std::string fixed4(double v) {
+    char b[64];
+    std::snprintf(b, sizeof b, "%.4f", v);
+    return b;
+}
+
+}  // namespace
+
+std::string emit_csv(std::span<const MetricsRecord> records) {
+    std::string out =
+        "policy,cache_budget,page_size,prefill_len,decode_steps,batch,layer_count,seed,"
+        "prefill_evicted,evictions_total,page_evictions,token_evictions,"
+        "block_table_updates,mean_fragmentation,max_fragmentation,"
+        "max_fragmentation_excl_newest,mean_deviation,p95_deviation,retained_bytes,"
+        "prefill_wall_ns,decode_wall_ns\n";
+    for (const auto& r : records) {
+        const std::string ints[] = {std::to_string(r.cache_budget), std::to_string(r.page_size),
+                                    std::to_string(r.prefill_len), std::to_string(r.decode_steps),
+                                    std::to_string(r.batch), std::to_string(r.layer_count), std::to_string(r.seed),
+                                    std::to_string(r.prefill_evicted), std::to_string(r.evictions_total),
+                                    std::to_string(r.page_evictions), std::to_string(r.token_evictions),
+                                    std::to_string(r.block_table_updates)};
+        out += csv_field(r.policy);
+        for (const auto& x : ints) out += "," + x;
+        for (const double d : {r.mean_fragmentation, r.max_fragmentation, r.max_fragmentation_excl_newest,
+                               r.mean_deviation, r.p95_deviation})
+            out += "," + csv_double(d);
+        out += "," + std::to_string(r.retained_bytes) + "," + std::to_string(r.prefill_wall_ns) + "," +
+               std::to_string(r.decode_wall_ns) + "\n";
+    }
+    return out;
+}
+
+std::string emit_jsonl(std::span<const StepRecord> steps) {
+    std::string out;
+    for (const auto& s : steps) {
+        out += "{\"run\":" + std::to_string(s.run) + ",\"seq\":" + std::to_string(s.sequence) +
+               ",\"layer\":" + std::to_string(s.layer) + ",\"step\":" + std::to_string(s.step) +
+               ",\"retained_len\":" + std::to_string(s.retained_len) + ",\"decision\":{\"kind\":";
+        switch (s.decision.kind) {
+        case EvictionDecision::Kind::None: out += "null"; break;
+        case EvictionDecision::Kind::Tokens: {
+            out += "\"tokens\",\"positions\":[";
+            for (std::size_t i = 0; i < s.decision.positions.size(); ++i)
+                out += (i ? "," : "") + std::to_string(s.decision.positions[i]);
+            out += "]";
+            break;
+        }
+        case EvictionDecision::Kind::Page:
+            out += "\"page\",\"logical_index\":" + std::to_string(s.decision.logical_index);
+            break;
+        }
+        out += "},\"fragmentation\":" + json_double(s.fragmentation) + ",\"deviation\":" +
+               json_double(s.deviation) + "}\n";
+    }
+    return out;
+}
+
+std::vector<SummaryRow> summarize(std::span<const MetricsRecord> records) {
+    if (records.empty()) throw EmptyInput("summarize requires at least one record");
+    std::map<std::string, SummaryRow> by_policy;
+    for (const auto& r : records) {
+        SummaryRow& row = by_policy[r.policy];
+        row.policy = r.policy;
+        row.runs += 1;
+        row.evictions_total += r.evictions_total;
+        row.block_table_updates += r.block_table_updates;
+        row.max_fragmentation_excl_newest = std::max(row.max_fragmentation_excl_newest,
+                                                     r.max_fragmentation_excl_newest);
+        row.mean_deviation += r.mean_deviation;
+    }
+    const auto paged = by_policy.find(std::string(to_string(PolicyKind::PagedEviction)));
+    const double paged_updates = paged == by_policy.end() ? 0.0 : static_cast<double>(paged->second.block_table_updates);
+    std::vector<SummaryRow> rows;
+    for (const PolicyKind kind : {PolicyKind::PagedEviction, PolicyKind::StreamingLlm, PolicyKind::InvKeyL2,
+                                  PolicyKind::KeyDiff, PolicyKind::FullCache}) {
+        const auto it = by_policy.find(std::string(to_string(kind)));
+        if (it == by_policy.end()) continue;
+        SummaryRow row = it->second;
+        row.mean_deviation /= static_cast<double>(row.runs);
+        row.cadence_ratio = paged_updates > 0.0 ? static_cast<double>(row.block_table_updates) / paged_updates
+                                                : std::numeric_limits<double>::quiet_NaN();
+        rows.push_back(std::move(row));
+    }
+    return rows;
+}
+
+std::string format_summary(std::span<const SummaryRow> rows) {
+    std::string out;
+    char line[256];
+    std::snprintf(line, sizeof line, "%-16s%6s%11s%15s%10s%22s%16s\n", "policy", "runs", "evictions", "table_updates",
+                  "cadence", "max_frag_excl_newest", "mean_deviation");
+    out += line;
+    for (const auto& r : rows) {
+        const std::string cad = std::isnan(r.cadence_ratio) ? std::string("n/a") : fixed4(r.cadence_ratio);
+        std::snprintf(line, sizeof line, "%-16s%6llu%11llu%15llu%10s%22s%16s\n", r.policy.c_str(),
+                      static_cast<unsigned long long>(r.runs), static_cast<unsigned long long>(r.evictions_total),
+                      static_cast<unsigned long long>(r.block_table_updates), cad.c_str(),
+                      fixed4(r.max_fragmentation_excl_newest).c_str(), fixed4(r.mean_deviation).c_str());
+        out += line;
+    }
+    return out;
+}
+
+std::vector<StepRecord> step_records(std::span<const pe_step_entry> entries, std::uint32_t page_size,
+                                     std::int64_t step, std::uint32_t run) {
+    std::vector<StepRecord> out;
+    out.reserve(entries.size());
+    for (const auto& e : entries) {
+        StepRecord r;
+        r.run = run;
+        r.step = step;
+        r.retained_len = static_cast<std::size_t>(e.retained_len);
+        r.decision = e.victim >= 0 ? EvictionDecision::page(static_cast<std::size_t>(e.victim), step)
+                                   : EvictionDecision::none(step);
+        // block_table.cpp:48-63
+        if (e.page_count > 0) {
+            const double slots = static_cast<double>(e.page_count) * page_size;
+            r.fragmentation = 1.0 - static_cast<double>(e.retained_len) / slots;
+        }
+        if (e.page_count > 1) {
+            const double slots = static_cast<double>(e.page_count - 1) * page_size;
+            r.fragmentation_excl_newest = 1.0 - static_cast<double>(e.retained_len - e.newest_fill) / slots;
+        }
+        r.deviation = std::numeric_limits<double>::quiet_NaN();
+        out.push_back(std::move(r));
+    }
+    return out;
 }
 
 }  // namespace pagedevict

@@ -66,6 +66,7 @@ struct pe_engine {
     int32_t* rank = nullptr;
     int32_t* work = nullptr;
     int32_t* victims = nullptr;
+    pe_step_entry* step_stage = nullptr;  // [n_tables] step-log staging for host destinations (lazy)
     int32_t* tickets = nullptr;
     int32_t* vpage = nullptr;           // per launch table released page id (or -1)
     unsigned long long* lb_status = nullptr;  // append look-back status words (one per CTA)
@@ -368,6 +369,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             cudaMemset(e->attn_tickets, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
             cudaMemset(e->lb_status, 0, sizeof(unsigned long long) * lb_words(n_tables)) != cudaSuccess ||
             cudaMemset(e->ctl, 0, sizeof(LaunchCtl)) != cudaSuccess ||
+            cudaMemset(e->victims, 0xFF, sizeof(int32_t) * n_tables) != cudaSuccess ||
             cudaMemset(s.positions, 0xFF, sizeof(int32_t) * (size_t)cap * s.B) != cudaSuccess ||
             cudaMemset(s.holes, 0, sizeof(unsigned long long) * (size_t)cap) != cudaSuccess ||
             cudaMemset(s.pages, 0, (size_t)cap * page_bytes) != cudaSuccess ||
@@ -455,7 +457,7 @@ pe_status pe_engine_destroy(pe_engine* e) {
                    e->work, e->victims, e->tickets, e->evict_scratch, e->tab_len, e->tab_tok0,
                    e->tab_pagebase, e->evicted_dev, e->part_o,
                    e->part_ml, e->out_stage, e->tab_keybase, e->keys, e->surv, e->lb_status,
-                   e->alloc_out, e->tok_out, e->attn_tickets, e->items, e->seq_units, e->seq_done, e->work_ctr, e->attend_logits, e->attend_out, e->attend_ws};
+                   e->alloc_out, e->tok_out, e->attn_tickets, e->items, e->seq_units, e->seq_done, e->work_ctr, e->attend_logits, e->attend_out, e->attend_ws, e->step_stage};
     for (void* p : dev) {
         if (p) cudaFree(p);
     }
@@ -793,6 +795,30 @@ pe_status pe_decode_step(pe_engine* e, int32_t layer_begin, int32_t n_layers, co
     pe_status r = pe_decode_append(e, layer_begin, n_layers, k_rows, v_rows, positions, stream);
     if (r != PE_OK) return r;
     return pe_decode_evict(e, layer_begin, n_layers, step, mode, victims, stream);
+}
+
+pe_status pe_step_log_capture(pe_engine* e, int32_t layer_begin, int32_t n_layers, const int32_t* victims,
+                              pe_step_entry* out, void* stream) {
+    if (e == nullptr || out == nullptr) return fail(PE_INVALID_ARG, "null argument");
+    const DevState& s = e->s;
+    if (layer_begin < 0 || n_layers <= 0 || layer_begin + n_layers > s.n_layers)
+        return fail(PE_INVALID_ARG, "layer range out of range");
+    if (victims != nullptr && !is_device_ptr(victims))
+        return fail(PE_INVALID_ARG, "victims must be a device array (or NULL for the engine's copy)");
+    cudaSetDevice(e->device);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TableSet ts{layer_begin, n_layers};
+    const int n = ts.size(s);
+    const bool out_dev = is_device_ptr(out);
+    if (!out_dev && e->step_stage == nullptr && dalloc(&e->step_stage, (size_t)s.n_tables) != cudaSuccess)
+        return fail(PE_CUDA_ERROR, "step-log staging allocation failed");
+    pe_step_entry* dst = out_dev ? out : e->step_stage;
+    step_log_kernel<<<(n + 255) / 256, 256, 0, st>>>(s, ts, victims ? victims : e->victims, dst);
+    pe_status r = check_launch(e, "step_log_kernel");
+    if (r != PE_OK) return r;
+    e->stats.kernel_launches += 1;
+    if (!out_dev) PE_CUDA(cudaMemcpyAsync(out, dst, sizeof(pe_step_entry) * n, cudaMemcpyDeviceToHost, st));
+    return PE_OK;
 }
 
 // ------------------------------------------------------------------ K3

@@ -92,6 +92,8 @@ __global__ void prompt_score_kernel(const float* k, int n, int w, int rule, cons
 __global__ void bitonic_step_kernel(double* score, long long* spos, int* sidx, int n_pad, int j, int k);
 __global__ void flag_first_kernel(const int* sidx, int k, uint8_t* flags);
 __global__ void invariants_tables_kernel(DevState s, int32_t* refs, unsigned long long* counters);
+// step-log capture (pe_step_log_capture): one entry per launch table
+__global__ void step_log_kernel(DevState s, TableSet ts, const int32_t* victims, pe_step_entry* out);
 __global__ void invariants_free_kernel(DevState s, int32_t* refs);
 __global__ void invariants_refs_kernel(DevState s, const int32_t* refs, unsigned long long* counters);
 __global__ void probe_read_kernel(const uint4* src, size_t n16, unsigned long long* sink);

@@ -491,4 +491,24 @@ __global__ void probe_copy_kernel(const uint4* __restrict__ src, uint4* __restri
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) dst[i] = __ldcs(src + i);
 }
 
+// ---------------------------------------------------------------------------
+// step_log_kernel: the engine-owned StepRecord fields of one decode step
+// (metrics.hpp:18-28) per launch table: retained_len, page_count, the newest
+// page's occupied slots (Page::fill, holes excluded) and the decision
+// (victims[i], the evicted logical page or -1), for the host-side emitters.
+__global__ void step_log_kernel(DevState s, TableSet ts, const int32_t* victims, pe_step_entry* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ts.size(s)) return;
+    const int t = ts.table(s, i);
+    const int np = s.num_pages[t];
+    int fill = 0;
+    if (np > 0) fill = page_fill(s, s.block_table[(int64_t)t * s.max_pages + np - 1], s.newest_fill[t]);
+    pe_step_entry e;
+    e.retained_len = s.retained[t];
+    e.page_count = np;
+    e.newest_fill = fill;
+    e.victim = victims[i];
+    out[i] = e;
+}
+
 }  // namespace pe

@@ -318,6 +318,24 @@ class PagedEvictionEngine:
         _check(self.lib.pe_get_stats(self.h, C.byref(out)))
         return out
 
+    def step_log(self, layer_begin, n_layers, victims=None, out=None, stream=None):
+        """Engine-owned StepRecord fields of every table of the layer range
+        after the preceding evict / decode_step (pe_step_log_capture):
+        [n, 4] int32 rows (retained_len, page_count, newest_fill, victim), in
+        launch order. victims: the device array given to that evict, or None
+        for the engine's copy. Returns a host array unless `out` (device) is
+        given; see steplog.step_records for the StepRecords."""
+        n = n_layers * self.geometry.n_seqs * self.tab_heads
+        host = out is None
+        if host:
+            out = np.zeros((n, 4), dtype=np.int32)
+        pv, va = _ptr(victims)
+        po, oa = _ptr(out)
+        _check(self.lib.pe_step_log_capture(self.h, layer_begin, n_layers, pv, po, _stream(stream)))
+        if host:
+            self.sync()
+        return out
+
     def check_invariants(self) -> dict:
         """Device-side structural invariants of every table and the pool
         (pe_check_invariants; selfcheck.cpp:19-75): returns the counts,

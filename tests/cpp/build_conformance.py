@@ -76,6 +76,31 @@ def build_scenario() -> tuple[Path, Path | None]:
     return b200, ref_out
 
 
+# the reference's JSON library (nlohmann/json, header-only; a pinned copy
+# ships in this image under cudnn_frontend's third-party tree)
+JSON_DIRS = [Path("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann")]
+
+
+def build_metrics_fmt() -> tuple[Path, Path | None]:
+    """metrics_fmt.cpp against the façade (tests/cpp/_build/metrics_fmt_b200)
+    and against the reference's metrics.cpp + JSON library
+    (oracle/_ref/metrics_fmt_ref), for the byte-identical emitter test."""
+    b200 = _cxx([HERE / "metrics_fmt.cpp"], OUT / "metrics_fmt_b200", [], shim_main=False)
+    ref_out = None
+    json_dir = next((d for d in JSON_DIRS if (d / "json.hpp").exists()), None)
+    if REF.exists() and json_dir is not None:
+        ref_dir = ROOT / "oracle" / "_ref"
+        ref_dir.mkdir(parents=True, exist_ok=True)
+        ref_out = ref_dir / "metrics_fmt_ref"
+        cmd = ["g++", "-std=c++20", "-O2", f"-I{REF / 'core' / 'include'}", f"-I{json_dir}",
+               str(HERE / "metrics_fmt.cpp"),
+               *[str(REF / "core" / "src" / f) for f in REF_CORE + ["metrics.cpp"]], "-lpthread", "-o", str(ref_out)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"g++ failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stderr[-8000:]}")
+    return b200, ref_out
+
+
 def build_all() -> None:
     from paper_2509_04377_b200 import _build
 
@@ -83,6 +108,7 @@ def build_all() -> None:
     build_facade_tests()
     build_reference_conformance()
     build_scenario()
+    build_metrics_fmt()
     build_examples()
 
 
