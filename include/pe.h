@@ -293,6 +293,20 @@ typedef enum pe_token_rule {
 pe_status pe_table_evict_token(pe_engine* eng, int32_t table, int32_t rule, int64_t arg, int32_t cache_budget,
                                int64_t newest_position, int64_t* victim_position, void* stream);
 
+/* Batched token eviction: the decode step of the StreamingLLM / InvKeyL2 /
+ * KeyDiff baselines (StreamingLlmPolicy / InvKeyL2Policy / KeyDiffPolicy::
+ * evict, policy.cpp:184-283) over every table of layers [layer_begin,
+ * layer_begin+n_layers), after the step's pe_decode_append. Every table
+ * holding more than the engine's budget C evicts one token by `rule`:
+ * PE_TOKEN_STREAMING (arg = sink count), PE_TOKEN_MAX_KEY_NORM or
+ * PE_TOKEN_KEY_DIFF; a page that drains is released (pushed in ascending
+ * table id after the append launch's pops). newest_positions [n_seqs] int64
+ * (host or device): the step's appended position, never a candidate.
+ * victim_positions (nullable, host or device) [n_layers*n_seqs*tab_heads]
+ * int64: the evicted position per table in launch order, or -1. */
+pe_status pe_decode_evict_tokens(pe_engine* eng, int32_t layer_begin, int32_t n_layers, int32_t rule, int64_t arg,
+                                 const int64_t* newest_positions, int64_t* victim_positions, void* stream);
+
 /* Evicted-slot masks (bit s = slot s is a hole) of pages [page_begin, +n_pages). */
 pe_status pe_read_page_holes(pe_engine* eng, int32_t page_begin, int32_t n_pages, uint64_t* holes);
 

@@ -314,12 +314,17 @@ class Reference:
         lib.ref_retained_len.argtypes = [C.c_void_p, C.c_size_t]
         lib.ref_fragmentation.restype = None
         lib.ref_fragmentation.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p]
+        lib.ref_append_token.restype = C.c_int
+        lib.ref_append_token.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, C.c_uint64]
+        lib.ref_policy_evict.restype = C.c_int
+        lib.ref_policy_evict.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64, C.c_int64,
+                                         C.POINTER(C.c_int), C.POINTER(C.c_int64)]
         lib.ref_free_count.restype = C.c_size_t
         lib.ref_free_count.argtypes = [C.c_void_p]
         lib.ref_read_table.argtypes = [C.c_void_p, C.c_size_t] + [C.c_void_p] * 5
         lib.ref_mirror_free_list.restype = C.c_size_t
         lib.ref_mirror_free_list.argtypes = [C.c_void_p, C.c_void_p]
-        lib.ref_drain_free_list.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_size_t)]
+        lib.ref_drain_free_list.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_size_t), C.c_int]
         lib.ref_attend_table.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_uint32,
                                          C.c_uint32, C.c_void_p]
         lib.ref_bench_decode_cycles.argtypes = [C.c_size_t, C.c_size_t, C.c_uint32, C.c_uint32,
@@ -463,6 +468,20 @@ class RefSession:
     def retained_len(self, t) -> int:
         return self.lib.ref_retained_len(self.h, t)
 
+    def append_token(self, t, k, v, position) -> None:
+        """BlockTable::append_token alone (phase 1 of a two-phase step)."""
+        k = np.ascontiguousarray(k, dtype=np.float32)
+        v = np.ascontiguousarray(v, dtype=np.float32)
+        self.ref._check(self.lib.ref_append_token(self.h, t, _ptr(k), _ptr(v), int(position)))
+
+    def policy_evict(self, t, newest, step) -> tuple[int, int]:
+        """The policy's evict after the append: (kind, victim position or
+        logical page, -1 if none)."""
+        kind, victim = C.c_int(0), C.c_int64(-1)
+        self.ref._check(self.lib.ref_policy_evict(self.h, t, int(newest), int(step), C.byref(kind),
+                                                  C.byref(victim)))
+        return kind.value, victim.value
+
     def fragmentation(self, t) -> tuple[float, float]:
         """(fragmentation_ratio, fragmentation_ratio_excluding_newest)."""
         out = (C.c_double * 2)()
@@ -495,10 +514,12 @@ class RefSession:
         n = self.lib.ref_mirror_free_list(self.h, _ptr(out))
         return out[:n].astype(np.int64)
 
-    def drain_free_list(self) -> np.ndarray:
+    def drain_free_list(self, check_mirror: bool = True) -> np.ndarray:
+        """Drains the real pool (allocate() until empty); with check_mirror
+        the order must equal the harness's free-list mirror."""
         out = np.zeros(max(self.capacity, 1), dtype=np.uint32)
         n = C.c_size_t()
-        self.ref._check(self.lib.ref_drain_free_list(self.h, _ptr(out), C.byref(n)))
+        self.ref._check(self.lib.ref_drain_free_list(self.h, _ptr(out), C.byref(n), int(check_mirror)))
         return out[: n.value].astype(np.int64)
 
     def attend(self, t, q, heads, dim):

@@ -167,6 +167,15 @@ KvVector kv_from(const float* k, const float* v, std::size_t w, std::uint64_t po
 
 }  // namespace
 
+// The policies' protected evict (policy.hpp:113-117), reached through a
+// member pointer formed in a derived class: the two-phase decode of the
+// engine's canonical batched order (all of a step's appends, then all
+// evictions) drives append_token and evict separately.
+struct EvictAccess : EvictionPolicy {
+    using Fn = EvictionDecision (EvictionPolicy::*)(BlockTable&, std::uint64_t, std::int64_t);
+    static Fn fn() { return &EvictAccess::evict; }
+};
+
 extern "C" {
 
 const char* ref_last_error() { return g_last_error.c_str(); }
@@ -335,6 +344,30 @@ int ref_decode_step(void* h, std::size_t t, const float* k, const float* v,
     });
 }
 
+// BlockTable::append_token (block_table.cpp:10-19) alone: phase 1 of a
+// two-phase decode step (no free-list mirror bookkeeping).
+int ref_append_token(void* h, std::size_t t, const float* k, const float* v, std::uint64_t position) {
+    auto* s = static_cast<Session*>(h);
+    return guarded([&] { s->tables.at(t).append_token(kv_from(k, v, s->width, position)); });
+}
+
+// The policy's evict after the append (phase 2): kind 0 None, 1 Tokens, 2
+// Page; *victim = the evicted position (Tokens, one per step for the
+// baselines) or logical page (Page), else -1.
+int ref_policy_evict(void* h, std::size_t t, std::uint64_t newest, std::int64_t step, int* kind,
+                     std::int64_t* victim) {
+    auto* s = static_cast<Session*>(h);
+    return guarded([&] {
+        EvictionPolicy& p = *s->policies.at(t);
+        const EvictionDecision d = (p.*EvictAccess::fn())(s->tables.at(t), newest, step);
+        *kind = static_cast<int>(d.kind);
+        *victim = -1;
+        if (d.kind == EvictionDecision::Kind::Tokens && !d.positions.empty())
+            *victim = static_cast<std::int64_t>(d.positions.front());
+        if (d.kind == EvictionDecision::Kind::Page) *victim = static_cast<std::int64_t>(d.logical_index);
+    });
+}
+
 std::size_t ref_page_count(void* h, std::size_t t) {
     return static_cast<Session*>(h)->tables.at(t).page_count();
 }
@@ -380,8 +413,9 @@ std::size_t ref_mirror_free_list(void* h, std::uint32_t* out) {
 }
 
 // Drains the real pool with allocate() (page_pool.cpp:24-33) and checks the
-// order against the mirror. Destroys the session's usefulness afterwards.
-int ref_drain_free_list(void* h, std::uint32_t* out, std::size_t* n) {
+// order against the mirror (check_mirror). Destroys the session's usefulness
+// afterwards.
+int ref_drain_free_list(void* h, std::uint32_t* out, std::size_t* n, int check_mirror) {
     auto* s = static_cast<Session*>(h);
     int st = guarded([&] {
         std::size_t i = 0;
@@ -390,7 +424,7 @@ int ref_drain_free_list(void* h, std::uint32_t* out, std::size_t* n) {
         }
         *n = i;
     });
-    if (st != RS_OK) return st;
+    if (st != RS_OK || !check_mirror) return st;  // (the two-phase calls keep no mirror)
     // allocate() pops from the back: out[i] must equal mirror[size-1-i].
     if (*n != s->mirror.size()) return RS_MIRROR_MISMATCH;
     for (std::size_t i = 0; i < *n; ++i) {

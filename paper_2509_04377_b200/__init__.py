@@ -23,6 +23,7 @@ from .engine import (  # noqa: F401
     PolicyKind,
     PoolExhausted,
     ScoreMode,
+    TokenRule,
     parse_policy_kind,
     to_string,
     DTYPE_BF16,

@@ -79,6 +79,7 @@ SIGNATURES = {
     "pe_prompt_select": (C.c_int, [c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_i32, c_vp]),
     "pe_check_invariants": (C.c_int, [c_vp, C.POINTER(PeInvariants)]),
     "pe_step_log_capture": (C.c_int, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
+    "pe_decode_evict_tokens": (C.c_int, [c_vp, c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "pe_probe_hbm": (C.c_int, [c_i32, c_i64, c_i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 

@@ -291,45 +291,6 @@ __device__ __forceinline__ bool evict_triggered(const DevState& s, int t) {
            s.retained[t] > s.C;
 }
 
-// Launch-level completion: every TABLE of the launch takes one ticket when it
-// is settled (a non-triggered table at once, a triggered one after its
-// finalize); whoever takes the launch's last ticket pushes the launch's
-// released pages on the free stack in ascending table id (release,
-// page_pool.cpp:35-38; canonical order DESIGN.md §1.6). `settled` is
-// block-uniform.
-__device__ __forceinline__ void push_victims_if_last(const DevState& s, int n, int32_t* vpage,
-                                                     unsigned long long grid_last, int settled) {
-    __shared__ int is_last;
-    __shared__ int scan_sm[33];
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) is_last = settled > 0 && (atomicAdd(s.grid_ctr, (unsigned long long)settled) + settled - 1 >= grid_last);
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-    // tiles of 16 consecutive entries per thread: independent loads, one
-    // block scan per tile (ascending table id = canonical push order)
-    const int top = *s.top;
-    int base = 0;
-    for (int t0 = 0; t0 < n; t0 += blockDim.x * 16) {
-        const int i0 = t0 + threadIdx.x * 16;
-        int v[16];
-        int cnt = 0;
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            v[u] = (i0 + u < n) ? __ldcg(vpage + i0 + u) : -1;
-            cnt += v[u] >= 0;
-        }
-        int total;
-        int k = base + block_excl_scan(cnt, scan_sm, &total);
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-            if (v[u] >= 0) s.stack[top + k++] = v[u];
-        base += total;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) *s.top = top + base;
-}
 
 // Page mean of a 16-slot page from the lane-pair scores S (pair r = slot r),
 // in slot order (score_pages -> page_score, importance.cpp:19-30); with holes,

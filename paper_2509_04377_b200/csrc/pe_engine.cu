@@ -117,6 +117,10 @@ struct pe_engine {
     // table-granular API (pe_table_*, pe_pool_*)
     int32_t* alloc_out = nullptr;
     int64_t* tok_out = nullptr;
+    int64_t* tok_newest = nullptr;   // [n_seqs] staged newest positions (batched token eviction, lazy)
+    size_t tok_newest_elems = 0;
+    int64_t* tok_victims = nullptr;  // [n_tables] victim positions for host destinations (lazy)
+    size_t tok_victims_elems = 0;
     int32_t* attn_tickets = nullptr;  // [n_tables] split-K completion tickets
     alignas(64) CUtensorMap pool_tmap;  // pages as [capacity*2*B rows][d] bf16, SWIZZLE_128B boxes of 32x64
     bool has_tmap = false;
@@ -457,7 +461,7 @@ pe_status pe_engine_destroy(pe_engine* e) {
                    e->work, e->victims, e->tickets, e->evict_scratch, e->tab_len, e->tab_tok0,
                    e->tab_pagebase, e->evicted_dev, e->part_o,
                    e->part_ml, e->out_stage, e->tab_keybase, e->keys, e->surv, e->lb_status,
-                   e->alloc_out, e->tok_out, e->attn_tickets, e->items, e->seq_units, e->seq_done, e->work_ctr, e->attend_logits, e->attend_out, e->attend_ws, e->step_stage};
+                   e->alloc_out, e->tok_out, e->attn_tickets, e->items, e->seq_units, e->seq_done, e->work_ctr, e->attend_logits, e->attend_out, e->attend_ws, e->step_stage, e->tok_newest, e->tok_victims};
     for (void* p : dev) {
         if (p) cudaFree(p);
     }
@@ -1177,6 +1181,45 @@ pe_status pe_table_evict_token(pe_engine* e, int32_t table, int32_t rule, int64_
     e->stats.kernel_launches += 1;
     if (victim_position != nullptr)
         PE_CUDA(cudaMemcpyAsync(victim_position, e->tok_out, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    return PE_OK;
+}
+
+pe_status pe_decode_evict_tokens(pe_engine* e, int32_t layer_begin, int32_t n_layers, int32_t rule, int64_t arg,
+                                 const int64_t* newest_positions, int64_t* victim_positions, void* stream) {
+    if (e == nullptr || newest_positions == nullptr) return fail(PE_INVALID_ARG, "null argument");
+    DevState& s = e->s;
+    if (layer_begin < 0 || n_layers <= 0 || layer_begin + n_layers > s.n_layers)
+        return fail(PE_INVALID_ARG, "layer range out of range");
+    if (rule != PE_TOKEN_STREAMING && rule != PE_TOKEN_MAX_KEY_NORM && rule != PE_TOKEN_KEY_DIFF)
+        return fail(PE_INVALID_ARG, "token rule (STREAMING, MAX_KEY_NORM or KEY_DIFF)");
+    if (s.B > 64) return fail(PE_INVALID_ARG, "unstructured eviction needs page_size <= 64");
+    cudaSetDevice(e->device);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TableSet ts{layer_begin, n_layers};
+    const int n = ts.size(s);
+    pe_status r;
+    const int64_t* dnew = newest_positions;
+    if (!is_device_ptr(newest_positions)) {
+        if ((r = ensure_t(&e->tok_newest, &e->tok_newest_elems, (size_t)s.n_seqs)) != PE_OK) return r;
+        PE_CUDA(cudaMemcpyAsync(e->tok_newest, newest_positions, sizeof(int64_t) * s.n_seqs, cudaMemcpyHostToDevice,
+                                st));
+        dnew = e->tok_newest;
+    }
+    const bool vic_dev = victim_positions != nullptr && is_device_ptr(victim_positions);
+    int64_t* dvic = vic_dev ? victim_positions : nullptr;
+    if (victim_positions != nullptr && !vic_dev) {
+        if ((r = ensure_t(&e->tok_victims, &e->tok_victims_elems, (size_t)s.n_tables)) != PE_OK) return r;
+        dvic = e->tok_victims;
+    }
+    s.holes_on = 1;  // from now on every kernel honours the hole masks
+    e->grid_tickets += (unsigned long long)n;  // one completion ticket per table
+    token_evict_batch_kernel<<<n, 256, sizeof(float) * s.w, st>>>(s, ts, rule, static_cast<long long>(arg), s.C,
+                                                                   dnew, dvic, e->vpage, e->grid_tickets - 1);
+    if ((r = check_launch(e, "token_evict_batch_kernel")) != PE_OK) return r;
+    e->stats.kernel_launches += 1;
+    e->stats.evict_calls += 1;
+    if (victim_positions != nullptr && !vic_dev)
+        PE_CUDA(cudaMemcpyAsync(victim_positions, dvic, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
     return PE_OK;
 }
 

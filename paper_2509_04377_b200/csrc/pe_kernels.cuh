@@ -86,6 +86,9 @@ __global__ void table_attend_kernel(DevState s, int32_t t, const float* q, int32
                                     float* out, double* weight_sums);
 __global__ void token_evict_kernel(DevState s, int32_t t, int32_t rule, long long arg, int32_t C, long long newest,
                                    float* mean, long long* out);
+__global__ void token_evict_batch_kernel(DevState s, TableSet ts, int32_t rule, long long arg, int32_t C,
+                                         const int64_t* newest_pos, int64_t* victims, int32_t* vpage,
+                                         unsigned long long grid_last);
 __global__ void prompt_mean_key_kernel(const float* k, int n, int w, float* mean, double* mnorm);
 __global__ void prompt_score_kernel(const float* k, int n, int w, int rule, const float* mean, const double* mnorm,
                                     const long long* pos, int n_pad, double* score, long long* spos, int* sidx);

@@ -192,8 +192,12 @@ __device__ __forceinline__ double row_sumsq_f(const uint8_t* row, int w, int dty
     return acc;
 }
 
-__global__ void token_evict_kernel(DevState s, int32_t t, int32_t rule, long long arg, int32_t C, long long newest,
-                                   float* mean, long long* out) {
+// One table, executed by a whole CTA (<= 256 threads; `mean` holds w floats
+// of shared or global scratch). Returns, on thread 0, the page released when
+// the victim's page drained (the caller pushes it on the free stack) or -1;
+// *out (thread 0) = victim position or -1.
+__device__ int token_evict_table(const DevState& s, int t, int rule, long long arg, int C, long long newest,
+                                 float* mean, long long* out) {
     __shared__ double sh_val[256];
     __shared__ int sh_x[256];
     __shared__ double sh_mnorm;
@@ -204,7 +208,7 @@ __global__ void token_evict_kernel(DevState s, int32_t t, int32_t rule, long lon
     const int64_t page_bytes = (int64_t)2 * s.B * s.pitch;
     if (C >= 0 && s.retained[t] <= C) {
         if (threadIdx.x == 0) *out = -1;
-        return;
+        return -1;
     }
     auto valid = [&](int x) {
         const int j = x / s.B, sl = x % s.B;
@@ -269,7 +273,7 @@ __global__ void token_evict_kernel(DevState s, int32_t t, int32_t rule, long lon
     sh_val[threadIdx.x] = bv;
     sh_x[threadIdx.x] = bx;
     __syncthreads();
-    if (threadIdx.x != 0) return;
+    if (threadIdx.x != 0) return -1;
     for (int i = 1; i < (int)blockDim.x; ++i) {
         if (sh_x[i] == 0x7FFFFFFF) continue;
         if (bx == 0x7FFFFFFF || sh_val[i] > bv || (sh_val[i] == bv && sh_x[i] < bx)) {
@@ -280,7 +284,7 @@ __global__ void token_evict_kernel(DevState s, int32_t t, int32_t rule, long lon
     if (bx == 0x7FFFFFFF) {
         if (rule == PE_TOKEN_AT_POSITION) set_status(s.status, PE_UNKNOWN_POSITION);
         *out = -1;
-        return;
+        return -1;
     }
     const int j = bx / s.B, sl = bx % s.B;
     const int page = row[j];
@@ -289,21 +293,53 @@ __global__ void token_evict_kernel(DevState s, int32_t t, int32_t rule, long lon
     s.retained[t] -= 1;
     const int cursor = (j == N - 1) ? nf : s.B;
     const int fill = page_fill(s, page, cursor);
-    if (fill == 0) {  // drained: release whole and close ranks
+    if (fill == 0) {  // drained: release whole (the caller pushes it) and close ranks
         s.holes[page] = 0ull;
-        const int top = *s.top;
-        s.stack[top] = page;
-        *s.top = top + 1;
         for (int k = j; k < N - 1; ++k) row[k] = row[k + 1];
         row[N - 1] = -1;
         s.num_pages[t] = N - 1;
         if (j == N - 1) s.newest_fill[t] = (N - 1 > 0) ? s.B : 0;
-    } else if (cursor == s.B) {  // keep the cached page mean of a full page current
+        return page;
+    }
+    if (cursor == s.B) {  // keep the cached page mean of a full page current
         double sum = 0.0;
         for (int k = 0; k < s.B; ++k)
             if (!slot_hole(s, page, k)) sum += s.token_scores[(int64_t)page * s.B + k];
         s.page_scores[page] = sum / static_cast<double>(fill);
     }
+    return -1;
+}
+
+__global__ void token_evict_kernel(DevState s, int32_t t, int32_t rule, long long arg, int32_t C, long long newest,
+                                   float* mean, long long* out) {
+    const int released = token_evict_table(s, t, rule, arg, C, newest, mean, out);
+    if (threadIdx.x == 0 && released >= 0) {  // release, page_pool.cpp:35-38
+        const int top = *s.top;
+        s.stack[top] = released;
+        *s.top = top + 1;
+    }
+}
+
+// Batched token eviction (the StreamingLLM / InvKeyL2 / KeyDiff decode step
+// over every table of a layer range, after the step's append launch): one
+// CTA per launch table, the table's mean key (KeyDiff) in shared memory;
+// newest_pos[seq] is the step's appended position. Pages that drain are
+// parked in vpage[y] and pushed by the grid's last CTA in ascending table
+// id (canonical order: the append launch's pops, then these pushes).
+__global__ void __launch_bounds__(256) token_evict_batch_kernel(DevState s, TableSet ts, int32_t rule, long long arg,
+                                                                int32_t C, const int64_t* newest_pos,
+                                                                int64_t* victims, int32_t* vpage,
+                                                                unsigned long long grid_last) {
+    extern __shared__ float mean_sm[];
+    __shared__ long long vpos;
+    const int y = blockIdx.x;
+    const int t = ts.table(s, y);
+    const int released = token_evict_table(s, t, rule, arg, C, newest_pos[ts.pos_index(s, y)], mean_sm, &vpos);
+    if (threadIdx.x == 0) {
+        vpage[y] = released;
+        if (victims) victims[y] = vpos;
+    }
+    push_victims_if_last(s, ts.size(s), vpage, grid_last, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -420,7 +456,10 @@ __global__ void invariants_tables_kernel(DevState s, int32_t* refs, unsigned lon
                 ++cnt;
             }
             last = pv;
-            if (j < N - 1 && cnt != s.B) ++not_full;
+            // page-aligned eviction: every non-newest page is full; with holes
+            // (unstructured eviction) a mapped page holds >= 1 token (a page
+            // that drains is released, block_table.cpp:33-46)
+            if (!s.holes_on ? (j < N - 1 && cnt != s.B) : cnt == 0) ++not_full;
         }
         occupied += cnt;
         order += bad_order;

@@ -156,6 +156,14 @@ class ScoreMode(enum.IntEnum):
     CACHED = 1     # K2c: page means cached when each page filled
 
 
+class TokenRule(enum.IntEnum):
+    """Victim rules of the unstructured baselines (pe_token_rule, pe.h)."""
+    AT_POSITION = 0   # BlockTable::evict_slot
+    STREAMING = 1     # StreamingLlmPolicy::evict (arg = sink count)
+    MAX_KEY_NORM = 2  # InvKeyL2Policy::evict
+    KEY_DIFF = 3      # KeyDiffPolicy::evict
+
+
 class Granularity(enum.IntEnum):
     PER_KV_HEAD = 0
     PER_LAYER = 1
@@ -316,6 +324,30 @@ class PagedEvictionEngine:
     def stats(self) -> _lib.PeStats:
         out = _lib.PeStats()
         _check(self.lib.pe_get_stats(self.h, C.byref(out)))
+        return out
+
+    def evict_tokens(self, layer_begin, n_layers, rule, arg, newest_positions, victims=None, stream=None):
+        """Decode step of the StreamingLLM / InvKeyL2 / KeyDiff baselines over
+        every table of the layer range, after the step's append_token
+        (pe_decode_evict_tokens; policy.cpp:184-283): tables over budget evict
+        one token by `rule`. With victims=True returns the evicted position
+        per table (launch order) or -1."""
+        want = victims is True
+        if want:
+            victims = np.zeros(n_layers * self.geometry.n_seqs * self.tab_heads, dtype=np.int64)
+        pn, na = _ptr(newest_positions)
+        pv, va = _ptr(victims)
+        _check(self.lib.pe_decode_evict_tokens(self.h, layer_begin, n_layers, int(rule), int(arg), pn, pv,
+                                               _stream(stream)))
+        if want:
+            self.sync()
+            return victims
+        return None
+
+    def page_holes(self) -> np.ndarray:
+        """Per page u64 mask of evicted slots (unstructured eviction)."""
+        out = np.zeros(self.capacity, dtype=np.uint64)
+        _check(self.lib.pe_read_page_holes(self.h, 0, self.capacity, C.c_void_p(out.ctypes.data)))
         return out
 
     def step_log(self, layer_begin, n_layers, victims=None, out=None, stream=None):
