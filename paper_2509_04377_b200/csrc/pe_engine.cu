@@ -708,7 +708,11 @@ pe_status launch_evict(pe_engine* e, const DevState& sc, const TableSet& ts, int
         // an all-layer launch), but enough CTAs for ~6 waves on small launches
         // (a per-layer launch of 512 tables gets 9 chunks of 29 pages).
         const int min_chunks = (sc.max_pages + kMaxPagesPerCta - 1) / kMaxPagesPerCta;
-        const int target_ctas = 28 * e->sm_count;
+        static const int ctas_per_sm = [] {
+            const char* v = std::getenv("PE_K2_CTAS_PER_SM");  // tuning override
+            return v ? std::max(1, std::atoi(v)) : 28;
+        }();
+        const int target_ctas = ctas_per_sm * e->sm_count;
         int chunks = std::max(min_chunks, (target_ctas + n - 1) / n);
         chunks = std::max(min_chunks, std::min(chunks, (sc.max_pages + 7) / 8));
         const int ppc = (sc.max_pages + chunks - 1) / chunks;
