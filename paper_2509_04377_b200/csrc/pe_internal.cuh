@@ -134,6 +134,17 @@ __device__ __forceinline__ double token_score_from_sumsq(double k2, double v2) {
     return vn / fmax(kn, kNormEps);
 }
 
+// The same score computed by a lane pair holding the same (k2, v2): lane q
+// takes one square root (q = 0: K, q = 1: V) and the pair exchanges them, so
+// each lane runs one IEEE double sqrt instead of two (bit-identical result).
+// Every lane of the warp must call it.
+__device__ __forceinline__ double pair_score_from_sumsq(double k2, double v2) {
+    const int q = threadIdx.x & 1;
+    const double r = sqrt(q ? v2 : k2);
+    const double o = __shfl_xor_sync(0xFFFFFFFFu, r, 1);
+    return (q ? r : o) / fmax(q ? o : r, kNormEps);
+}
+
 // ------------------------------------------------------------------ warp/cta scans
 __device__ __forceinline__ int warp_incl_scan(int v) {
     const int lane = threadIdx.x & 31;

@@ -176,13 +176,13 @@ __device__ __forceinline__ double pair_token_score_bf16(const uint8_t* krow, con
     vp += __shfl_xor_sync(0xFFFFFFFFu, vp, 1);
     kmin = min(kmin, __shfl_xor_sync(0xFFFFFFFFu, kmin, 1));
     vmin = min(vmin, __shfl_xor_sync(0xFFFFFFFFu, vmin, 1));
-    if (!valid) return 0.0;
     const double s768 = two_pow_768();
     double k2 = kp * s768;
     double v2 = vp * s768;
-    if (!bf16_sum_certified(kp, kmin)) k2 = row_sumsq_seq_bf16(krow, W);
-    if (!bf16_sum_certified(vp, vmin)) v2 = row_sumsq_seq_bf16(vrow, W);
-    return token_score_from_sumsq(k2, v2);
+    if (valid && !bf16_sum_certified(kp, kmin)) k2 = row_sumsq_seq_bf16(krow, W);
+    if (valid && !bf16_sum_certified(vp, vmin)) v2 = row_sumsq_seq_bf16(vrow, W);
+    const double S = pair_score_from_sumsq(k2, v2);  // all lanes: one sqrt each
+    return valid ? S : 0.0;
 }
 
 // fp32: lane 0 of the pair sums the K row, lane 1 the V row, sequentially
