@@ -505,6 +505,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     int64_t total_pages = 0;
     int64_t total_keys = 0;
     int max_len = 0;
+    int max_short = 0;  // longest table the CTA-per-table select can hold
     // the pinned per-table arrays are still being copied by the previous call
     // until its metadata event fires
     PE_CUDA(cudaEventSynchronize(e->ev_meta));
@@ -516,6 +517,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
         if (np > s.max_pages)
             return fail(PE_INVALID_ARG, "prefill of " + std::to_string(L) + " tokens exceeds max_pages_per_table");
         max_len = std::max(max_len, L);
+        if (L <= kSelectCtaMaxLen) max_short = std::max(max_short, L);
         for (int h = 0; h < H; ++h) {
             const int i = q * H + h;
             e->h_tab_len[i] = L;
@@ -570,6 +572,14 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     const bool force_cluster = sel_env != nullptr && std::strcmp(sel_env, "cluster") == 0;
     const bool use_cta_select = max_len <= kSelectCtaMaxLen && !force_cluster;
     a.chunk_cap = use_cta_select ? max_len : chunk_cap;  // keys held in smem per CTA
+    a.cta_len_max = 0x7FFFFFFF;
+    a.cluster_len_min = -1;
+    // Mixed lengths with some tables too long for the CTA select: the short
+    // tables still take the CTA select, only the long ones the cluster select
+    // (each kernel skips the other's tables). PE_SELECT_MIXED=0 disables it.
+    const char* mx = std::getenv("PE_SELECT_MIXED");
+    const bool mixed_select = !use_cta_select && !force_cluster && max_short > 0 &&
+                              !(mx != nullptr && std::strcmp(mx, "0") == 0);
     if (total_pages > INT32_MAX) return fail(PE_POOL_EXHAUSTED, "page pool exhausted");
     plan_prefill_kernel<<<1, 1024, 0, st>>>(s, a, static_cast<int32_t>(total_pages), e->ctl);
     // Opt-in (PE_PREFILL_FUSED=1): the persistent single-launch variant. On
@@ -667,6 +677,17 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
             const size_t sel_smem =
                 (((size_t)max_len * 4 + 15) & ~size_t(15)) + kSelHistCopies * 2048 * 4 + kSelCandCap * 4;
             prefill_select_cta_kernel<<<aw.n_tab, 1024, sel_smem, sw>>>(s, aw, e->ctl);
+        } else if (mixed_select) {
+            PrefillArgs ac = aw;  // tables <= kSelectCtaMaxLen
+            ac.chunk_cap = max_short;
+            ac.cta_len_max = kSelectCtaMaxLen;
+            const size_t sel_smem =
+                (((size_t)max_short * 4 + 15) & ~size_t(15)) + kSelHistCopies * 2048 * 4 + kSelCandCap * 4;
+            prefill_select_cta_kernel<<<aw.n_tab, 1024, sel_smem, sw>>>(s, ac, e->ctl);
+            PrefillArgs al = aw;  // the longer tables
+            al.cluster_len_min = kSelectCtaMaxLen;
+            prefill_select_kernel<<<dim3(kPrefillCluster, aw.n_tab), kPackThreads, pack_smem, sw>>>(s, al, e->ctl);
+            e->stats.kernel_launches += 1;
         } else {
             prefill_select_kernel<<<dim3(kPrefillCluster, aw.n_tab), kPackThreads, pack_smem, sw>>>(s, aw, e->ctl);
         }

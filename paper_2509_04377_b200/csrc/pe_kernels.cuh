@@ -29,6 +29,8 @@ struct PrefillArgs {
     int32_t seq_begin, layer;
     int32_t chunk_cap;                   // max tokens per CTA (keys smem capacity)
     int32_t score_tokens;                // tokens (x all heads) per score CTA
+    int32_t cta_len_max;                 // CTA select: tables longer than this are skipped
+    int32_t cluster_len_min;             // cluster select: tables this short or shorter are skipped
 };
 
 __global__ void evict_cached_kernel(DevState s, TableSet ts, double* scratch, int32_t* vpage, int32_t* victims,

@@ -202,6 +202,7 @@ __global__ void __cluster_dims__(kPrefillCluster, 1, 1) __launch_bounds__(kPackT
     __shared__ int bc[8];
 
     if (ctl->abort) return;  // uniform for the whole grid
+    if (a.tab_len[blockIdx.y] <= a.cluster_len_min) return;  // mixed lengths: the CTA select's table (whole cluster)
     const int CL = kPrefillCluster;
     const int r = static_cast<int>(cluster.block_rank());
     const int i = blockIdx.y;
@@ -796,6 +797,7 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
 __global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
     extern __shared__ __align__(16) uint8_t smem[];
     if (ctl->abort) return;
+    if (a.tab_len[blockIdx.x] > a.cta_len_max) return;  // mixed lengths: the cluster select's table
     select_table_cta(s, a, blockIdx.x, smem, ctl);
 }
 

@@ -344,6 +344,28 @@ def test_prefill_long_context_cluster_select():
     check(eng, orc, "long: ")
 
 
+@pytest.mark.parametrize("mixed", ["1", "0"])
+def test_prefill_mixed_lengths_split_select(mixed, monkeypatch):
+    """One prefill call with tables on both sides of the CTA select's limit
+    (34816 tokens): the short ones take the CTA select, the long ones the
+    cluster select (PE_SELECT_MIXED=0: all of them the cluster select).
+    Tie-heavy keys on one sequence; identity tables (L <= C) included."""
+    monkeypatch.setenv("PE_SELECT_MIXED", mixed)
+    rng = np.random.default_rng(34816)
+    B, C, d, H = 16, 2048, 128, 2
+    lens = np.array([40000, 1500, 34816, 9000, 34817, 700])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=len(lens), n_layers=1, H=H, d=d, B=B, C=C, dtype=oracle.BF16)
+    k, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+    v, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+    kg, _ = grid_kv(rng, (lens[3], H, d), oracle.BF16)
+    k[cu[3]:cu[4]] = kg
+    ev = eng.prefill_compress(0, dev(k), dev(v), cu, evicted_counts=True)
+    _, oev = orc.prefill(0, k, v, cu)
+    np.testing.assert_array_equal(ev, oev)
+    check(eng, orc, "mixed: ")
+
+
 @pytest.mark.parametrize("mode", [0, 1])
 def test_invariants_hold_after_prefill_and_decode(mode):
     """pe_check_invariants on a decoded engine: no violation, pages mapped +
