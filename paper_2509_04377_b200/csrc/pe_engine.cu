@@ -412,6 +412,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             !allow(reinterpret_cast<const void*>(attention_split_kernel), &e->max_dyn_attn) ||
             !allow(attention_mma_fn(64), &mma64) || !allow(attention_mma_fn(128), &mma128) ||
             !allow(reinterpret_cast<const void*>(prefill_select_cta_kernel), &sel_cta) ||
+            !allow(reinterpret_cast<const void*>(prefill_select_stream_kernel), &sel_cta) ||
             !allow(prefill_fused_fn(e->variant), &sel_cta)) {
             cudaGetLastError();
             return cleanup_fail(fail(PE_CUDA_ERROR, "cudaFuncSetAttribute(max dynamic smem) failed"));
@@ -580,6 +581,11 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     const char* mx = std::getenv("PE_SELECT_MIXED");
     const bool mixed_select = !use_cta_select && !force_cluster && max_short > 0 &&
                               !(mx != nullptr && std::strcmp(mx, "0") == 0);
+    // Tables over the limit take the CTA select with its high words streamed
+    // from global memory (one CTA per table); PE_SELECT_LONG=cluster keeps the
+    // 8-CTA cluster select for them.
+    const char* lg = std::getenv("PE_SELECT_LONG");
+    const bool stream_long = !use_cta_select && !force_cluster && !(lg != nullptr && std::strcmp(lg, "cluster") == 0);
     if (total_pages > INT32_MAX) return fail(PE_POOL_EXHAUSTED, "page pool exhausted");
     plan_prefill_kernel<<<1, 1024, 0, st>>>(s, a, static_cast<int32_t>(total_pages), e->ctl);
     // Opt-in (PE_PREFILL_FUSED=1): the persistent single-launch variant. On
@@ -650,7 +656,9 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     // The canonical page reservation (plan) is made once for the whole call.
     // (the cluster select of long tables is kept out of the wave overlap: its
     // 8-CTA clusters co-schedule badly next to another stream's kernels)
-    int waves = !use_cta_select ? 1 : (n_seqs >= 2 ? 2 : 1);
+    const char* lw = std::getenv("PE_LONG_WAVES");  // sequence waves with the streamed long-table select
+    const bool long_waves = stream_long && lw != nullptr && std::strcmp(lw, "1") == 0;
+    int waves = (!use_cta_select && !long_waves) ? 1 : (n_seqs >= 2 ? 2 : 1);
     if (const char* wv = std::getenv("PE_PREFILL_WAVES")) waves = std::max(1, std::min(n_seqs, std::atoi(wv)));
     if (waves > 1) {
         PE_CUDA(cudaEventRecord(e->ev_fork, st));
@@ -677,6 +685,20 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
             const size_t sel_smem =
                 (((size_t)max_len * 4 + 15) & ~size_t(15)) + kSelHistCopies * 2048 * 4 + kSelCandCap * 4;
             prefill_select_cta_kernel<<<aw.n_tab, 1024, sel_smem, sw>>>(s, aw, e->ctl);
+        } else if (stream_long) {
+            if (max_short > 0) {  // tables <= kSelectCtaMaxLen: hi words in shared memory
+                PrefillArgs ac = aw;
+                ac.chunk_cap = max_short;
+                ac.cta_len_max = kSelectCtaMaxLen;
+                const size_t sel_smem =
+                    (((size_t)max_short * 4 + 15) & ~size_t(15)) + kSelHistCopies * 2048 * 4 + kSelCandCap * 4;
+                prefill_select_cta_kernel<<<aw.n_tab, 1024, sel_smem, sw>>>(s, ac, e->ctl);
+                e->stats.kernel_launches += 1;
+            }
+            PrefillArgs al = aw;
+            al.cluster_len_min = max_short > 0 ? kSelectCtaMaxLen : -1;
+            const size_t st_smem = (size_t)kSelHistCopies * 2048 * 4 + (size_t)kSelCandCapStream * 4;
+            prefill_select_stream_kernel<<<aw.n_tab, 1024, st_smem, sw>>>(s, al, e->ctl);
         } else if (mixed_select) {
             PrefillArgs ac = aw;  // tables <= kSelectCtaMaxLen
             ac.chunk_cap = max_short;

@@ -41,6 +41,8 @@ __global__ void prefill_select_cta_kernel(DevState s, PrefillArgs a, const Launc
 constexpr int kSelHistCopies = 8;        // private histogram copies in the CTA select kernel
 constexpr int kSelCandCap = 4096;        // boundary-bin candidates compacted after the first radix pass
 constexpr int kSelectCtaMaxLen = 34816;  // CTA-per-table select: 4 B of smem per token + 64 KB histograms + 16 KB candidates
+constexpr int kSelCandCapStream = 16384;  // candidates of the streamed CTA select (no hi words in smem)
+__global__ void prefill_select_stream_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 __global__ void prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 // persistent fused prefill (score units + per-table select/copy), pe_prefill.cu
 void launch_prefill_fused_any(int variant, int grid, size_t smem, cudaStream_t st, const DevState& s,

@@ -479,6 +479,11 @@ __device__ __forceinline__ int block_find_digit(const uint32_t* hist, int nbins,
 
 // Select of launch table i by the whole CTA (1024 threads); `smem` is the
 // dynamic shared memory (hi words, histogram copies, candidates).
+// SMEM_HI: the table's high key words are held in shared memory (tables up to
+// kSelectCtaMaxLen tokens); otherwise every pass reads them from the keys in
+// global memory (tables of any length, e.g. cfg5's 128K-token tables), with a
+// larger candidate list in the shared memory the hi words would have used.
+template <bool SMEM_HI>
 __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillArgs& a, int i, uint8_t* smem,
                                               const LaunchCtl* ctl) {
     __shared__ uint32_t hist[2048];  // reduced histogram
@@ -494,14 +499,20 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
     const int seq = a.seq_begin + i / s.tab_heads;
     const int t = (seq * s.n_layers + a.layer) * s.tab_heads + h;
     const int B = s.B;
-    uint32_t* hi = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* hi = reinterpret_cast<uint32_t*>(smem);  // SMEM_HI only
+    const int cand_cap = SMEM_HI ? kSelCandCap : kSelCandCapStream;
     // kSelHistCopies private histograms (warp w -> copy w % kSelHistCopies):
     // the early digits of a table's keys are concentrated in a few bins, so a
     // single histogram would serialise every warp's atomics on them
-    uint32_t* hcopy = reinterpret_cast<uint32_t*>(smem + (((size_t)a.chunk_cap * 4 + 15) & ~size_t(15)));
+    uint32_t* hcopy =
+        reinterpret_cast<uint32_t*>(SMEM_HI ? smem + (((size_t)a.chunk_cap * 4 + 15) & ~size_t(15)) : smem);
     uint32_t* my_hist = hcopy + ((threadIdx.x >> 5) % kSelHistCopies) * 2048;
-    int32_t* cand = reinterpret_cast<int32_t*>(hcopy + kSelHistCopies * 2048);  // [kSelCandCap]
+    int32_t* cand = reinterpret_cast<int32_t*>(hcopy + kSelHistCopies * 2048);  // [cand_cap]
     const unsigned long long* gk = a.keys + a.tab_keybase[i];
+    auto HI = [&](int j) -> uint32_t {
+        if constexpr (SMEM_HI) return hi[j];
+        else return static_cast<uint32_t>(__ldcg(gk + j) >> 32);
+    };
     int32_t* surv = a.surv + (int64_t)a.tab_pagebase[i] * B;
 
     // ---- 0. pivot window from a sorted sample of 1024 high words: every key
@@ -567,7 +578,7 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
             const bool in = j < w_end;
             const uint32_t w = static_cast<uint32_t>(kv[u] >> 32);
             if (in) {
-                hi[j] = w;
+                if constexpr (SMEM_HI) hi[j] = w;
                 hmin = min(hmin, w);
                 hmax = max(hmax, w);
             }
@@ -609,7 +620,7 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
                 over |= w_seg[w] > kSegCap;
                 c += w_seg[w];
             }
-            win_ok = !over && c <= kSelCandCap && b < E && E <= b + c;
+            win_ok = !over && c <= cand_cap && b < E && E <= b + c;
             below_sum = b;
             n_cand = c;
         }
@@ -661,7 +672,7 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
             const int n_iter = use_cand ? (n_cand + nthr - 1) / nthr * nthr : n_round_all;
             for (int x = tid; x < n_iter; x += nthr) {
                 const int j = use_cand ? (x < n_cand ? cand[x] : L) : x;
-                const unsigned int w = j < L ? hi[j] : 0u;
+                const unsigned int w = j < L ? HI(j) : 0u;
                 const bool act = j < L && (bitpos == 32 || (w >> bitpos) == hp);
                 hist_add(hh, (w >> shift) & dmask, act);
             }
@@ -673,12 +684,12 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
             bitpos = shift;
             fshift = 32 + shift;
             done = bc[2] == k_rem;
-            if (!done && !use_cand && bc[2] <= kSelCandCap) {
+            if (!done && !use_cand && bc[2] <= cand_cap) {
                 // compact the chosen bin (warp-aggregated appends)
                 if (tid == 0) n_cand = 0;
                 __syncthreads();
                 for (int j = tid; j < n_round_all; j += nthr) {
-                    const bool in = j < L && (hi[j] >> bitpos) == hp;
+                    const bool in = j < L && (HI(j) >> bitpos) == hp;
                     const unsigned m = __ballot_sync(0xFFFFFFFFu, in);
                     int base = 0;
                     if ((tid & 31) == 0 && m) base = atomicAdd(&n_cand, __popc(m));
@@ -707,7 +718,7 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
                 const int n_iter = use_cand ? (n_cand + nthr - 1) / nthr * nthr : n_round_all;
                 for (int x = tid; x < n_iter; x += nthr) {
                     const int j = use_cand ? (x < n_cand ? cand[x] : L) : x;
-                    bool act = j < L && hi[j] == hp;
+                    bool act = j < L && HI(j) == hp;
                     unsigned int lw = 0u;
                     if (act) {
                         lw = static_cast<unsigned int>(__ldcg(gk + j));
@@ -737,17 +748,18 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
         less = false;
         tie = false;
         if (E == 0) return;
-        if (hi[j] < p_lo || hi[j] > p_hi) {  // outside the candidate window
-            less = hi[j] < p_lo;
+        const unsigned int hj = HI(j);
+        if (hj < p_lo || hj > p_hi) {  // outside the candidate window
+            less = hj < p_lo;
             return;
         }
         if (fshift >= 32) {
-            const unsigned long long top = static_cast<unsigned long long>(hi[j]) >> (fshift - 32);
+            const unsigned long long top = static_cast<unsigned long long>(hj) >> (fshift - 32);
             less = top < prefix;
             tie = top == prefix;
         } else {
             const unsigned long long hp64 = prefix >> (32 - fshift);
-            const unsigned long long hw = hi[j];
+            const unsigned long long hw = hj;
             if (hw != hp64) {
                 less = hw < hp64;
             } else {
@@ -798,7 +810,18 @@ __global__ void __launch_bounds__(1024, 1) prefill_select_cta_kernel(DevState s,
     extern __shared__ __align__(16) uint8_t smem[];
     if (ctl->abort) return;
     if (a.tab_len[blockIdx.x] > a.cta_len_max) return;  // mixed lengths: the cluster select's table
-    select_table_cta(s, a, blockIdx.x, smem, ctl);
+    select_table_cta<true>(s, a, blockIdx.x, smem, ctl);
+}
+
+// Tables longer than kSelectCtaMaxLen: the same CTA-per-table select with the
+// high key words read from global memory (grid = launch tables; tables of at
+// most `cluster_len_min` tokens are skipped: they take the shared-memory one).
+__global__ void __launch_bounds__(1024, 1) prefill_select_stream_kernel(DevState s, PrefillArgs a,
+                                                                        const LaunchCtl* ctl) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    if (ctl->abort) return;
+    if (a.tab_len[blockIdx.x] <= a.cluster_len_min) return;
+    select_table_cta<false>(s, a, blockIdx.x, smem, ctl);
 }
 
 // ---------------------------------------------------------------------------
@@ -931,7 +954,7 @@ __global__ void __launch_bounds__(1024, 1) prefill_fused_kernel(DevState s, Pref
             }
             __syncthreads();
             const int i = sq * H + idx;
-            select_table_cta(s, a, i, smem, ctl);
+            select_table_cta<true>(s, a, i, smem, ctl);
             __threadfence();
             __syncthreads();
             const int L = a.tab_len[i];

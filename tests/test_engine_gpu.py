@@ -328,9 +328,13 @@ def test_decode_pool_exhaustion_matches_serial_semantics():
 
 
 @pytest.mark.slow
-def test_prefill_long_context_cluster_select():
-    """Tables longer than the CTA select limit (49152 tokens) take the
-    cluster select kernel: 2 sequences x 2 KV heads at 60000 tokens."""
+@pytest.mark.parametrize("long_path", ["stream", "cluster"])
+def test_prefill_long_context_cluster_select(long_path, monkeypatch):
+    """Tables longer than the CTA select limit (34816 tokens): the streamed
+    CTA select (default) or the cluster select (PE_SELECT_LONG=cluster),
+    2 sequences x 2 KV heads at 60000 / 50001 tokens."""
+    if long_path == "cluster":
+        monkeypatch.setenv("PE_SELECT_LONG", "cluster")
     rng = np.random.default_rng(60000)
     B, C, d, H = 16, 4096, 128, 2
     lens = np.array([60000, 50001])
@@ -344,13 +348,16 @@ def test_prefill_long_context_cluster_select():
     check(eng, orc, "long: ")
 
 
-@pytest.mark.parametrize("mixed", ["1", "0"])
-def test_prefill_mixed_lengths_split_select(mixed, monkeypatch):
+@pytest.mark.parametrize("long_path,mixed", [("stream", "1"), ("cluster", "1"), ("cluster", "0")])
+def test_prefill_mixed_lengths_split_select(long_path, mixed, monkeypatch):
     """One prefill call with tables on both sides of the CTA select's limit
-    (34816 tokens): the short ones take the CTA select, the long ones the
-    cluster select (PE_SELECT_MIXED=0: all of them the cluster select).
+    (34816 tokens): the short ones take the shared-memory CTA select, the long
+    ones the streamed CTA select (default) or the cluster select
+    (PE_SELECT_LONG=cluster; with PE_SELECT_MIXED=0 every table takes it).
     Tie-heavy keys on one sequence; identity tables (L <= C) included."""
     monkeypatch.setenv("PE_SELECT_MIXED", mixed)
+    if long_path == "cluster":
+        monkeypatch.setenv("PE_SELECT_LONG", "cluster")
     rng = np.random.default_rng(34816)
     B, C, d, H = 16, 2048, 128, 2
     lens = np.array([40000, 1500, 34816, 9000, 34817, 700])
