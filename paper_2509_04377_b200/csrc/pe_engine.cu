@@ -571,7 +571,9 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     // PE_SELECT=cluster forces the cluster kernel (tests exercise both paths)
     const char* sel_env = std::getenv("PE_SELECT");
     const bool force_cluster = sel_env != nullptr && std::strcmp(sel_env, "cluster") == 0;
-    const bool use_cta_select = max_len <= kSelectCtaMaxLen && !force_cluster;
+    const bool force_stream = sel_env != nullptr && std::strcmp(sel_env, "stream") == 0;  // A/B: every table streamed
+    if (force_stream) max_short = 0;
+    const bool use_cta_select = max_len <= kSelectCtaMaxLen && !force_cluster && !force_stream;
     a.chunk_cap = use_cta_select ? max_len : chunk_cap;  // keys held in smem per CTA
     a.cta_len_max = 0x7FFFFFFF;
     a.cluster_len_min = -1;
