@@ -42,23 +42,26 @@ def engine_retained(eng, holes, t, bt, npg, nf, pos):
 
 
 @pytest.mark.parametrize("rule", [pe.TokenRule.STREAMING, pe.TokenRule.MAX_KEY_NORM, pe.TokenRule.KEY_DIFF])
-@pytest.mark.parametrize("dtype", [oracle.F32, oracle.BF16])
-def test_batched_token_eviction_matches_reference(reference, rule, dtype):
-    rng = np.random.default_rng(100 + int(rule) * 7 + dtype)
-    B, C, d, H, S, NL = 8, 32, 16, 2, 3, 2
+@pytest.mark.parametrize("dtype,gran", [(oracle.F32, 0), (oracle.BF16, 0), (oracle.BF16, 1)])
+def test_batched_token_eviction_matches_reference(reference, rule, dtype, gran):
+    """gran 1: PER_LAYER tables (one table per (sequence, layer), rows of all
+    KV heads, width H*d)."""
+    rng = np.random.default_rng(100 + int(rule) * 7 + dtype + 31 * gran)
+    B, C, d, Hkv, S, NL = 8, 32, 16, 2, 3, 2
+    H, w = (1, Hkv * d) if gran else (Hkv, d)  # table heads, table row width
     lens = np.array([C, 5, C - 9])  # identity prefill (L <= C) for every policy
     cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
-    geo = pe.EngineGeometry(n_seqs=S, n_layers=NL, n_kv_heads=H, head_dim=d, dtype=dtype,
-                            max_pages_per_table=C // B + 8)
+    geo = pe.EngineGeometry(n_seqs=S, n_layers=NL, n_kv_heads=Hkv, head_dim=d, dtype=dtype,
+                            granularity=pe.Granularity(gran), max_pages_per_table=C // B + 8)
     # the batched baselines run on a FullCache-kind engine (identity prefill,
     # no PagedEviction trigger); the budget C drives pe_decode_evict_tokens
     eng = pe.PagedEvictionEngine(geo, pe.PolicyConfig(cache_budget=C, page_size=B,
                                                       kind=pe.PolicyKind.FullCache))
-    sess = reference.session(eng.capacity, B, C, eng.n_tables, d, KIND[rule])
+    sess = reference.session(eng.capacity, B, C, eng.n_tables, w, KIND[rule])
     tid = lambda s, l, h: (s * NL + l) * H + h  # noqa: E731
     for layer in range(NL):
-        k, k32 = random_kv(rng, (cu[-1], H, d), dtype)
-        v, v32 = random_kv(rng, (cu[-1], H, d), dtype)
+        k, k32 = random_kv(rng, (cu[-1], H, w), dtype)
+        v, v32 = random_kv(rng, (cu[-1], H, w), dtype)
         eng.prefill_compress(layer, dev(k), dev(v), cu)
         for s in range(S):
             for h in range(H):
@@ -68,8 +71,8 @@ def test_batched_token_eviction_matches_reference(reference, rule, dtype):
     updates = 0
     for step in range(1, 3 * B + 6):
         gen = grid_kv if step % 3 == 0 else random_kv  # ties in ||K|| and cosine
-        k, k32 = gen(rng, (NL, S, H, d), dtype)
-        v, v32 = random_kv(rng, (NL, S, H, d), dtype)
+        k, k32 = gen(rng, (NL, S, H, w), dtype)
+        v, v32 = random_kv(rng, (NL, S, H, w), dtype)
         eng.append_token(0, NL, dev(k), dev(v), dev(pos))
         vic = eng.evict_tokens(0, NL, rule, SINKS, dev(pos), victims=True)
         order = [(s, li, h) for s in range(S) for li in range(NL) for h in range(H)]
