@@ -53,8 +53,9 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
                                                                  const int64_t* __restrict__ positions,
                                                                  unsigned long long* lb_status,
                                                                  unsigned long long* lb_group, LaunchCtl* ctl,
-                                                                 unsigned long long ticket_base, int epoch) {
-    __shared__ int sh_lid, sh_warp_cnt[kAppendThreads / 32], sh_prefix, sh_pop_base;
+                                                                 unsigned long long ticket_base, int epoch,
+                                                                 int fast_ok) {
+    __shared__ int sh_lid, sh_warp_cnt[kAppendThreads / 32], sh_prefix, sh_pop_base, sh_fast;
 #ifdef PE_K0_TRACE
     unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int polls = 0;
@@ -68,7 +69,13 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
     const int nw = kAppendThreads / 32;
     const int n = ts.size(s);
     const int n_ctas = (n + 16 * nw - 1) / (16 * nw);
-    if (threadIdx.x == 0) sh_lid = static_cast<int>(atomicAdd(s.grid_ctr, 1ull) - ticket_base);
+    if (threadIdx.x == 0) {
+        sh_lid = static_cast<int>(atomicAdd(s.grid_ctr, 1ull) - ticket_base);
+        // no-pop fast path: the previous append over the same tables (and no
+        // other table operation since, fast_ok) flagged no table as popping
+        // on this launch, so every pop rank is 0 and the look-back is skipped
+        sh_fast = fast_ok && *reinterpret_cast<volatile unsigned int*>(&ctl->pop_flag) != static_cast<unsigned>(epoch);
+    }
     __syncthreads();
     PE_TR(1);
     const int lid = sh_lid;
@@ -95,7 +102,16 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
     if (lane == 0) sh_warp_cnt[wid] = __popc(pop_mask);
     __syncthreads();
     PE_TR(2);
-    if (wid == 0) {
+    const bool fast = sh_fast;
+    if (fast) {
+        if (threadIdx.x == 0) {
+            int local = 0;
+            for (int w = 0; w < nw; ++w) local += sh_warp_cnt[w];
+            if (local != 0) set_status(s.status, PE_INVALID_STATE);  // a mispredicted pop: never served below
+            sh_prefix = 0;
+            sh_pop_base = 0x7FFFFFFF;
+        }
+    } else if (wid == 0) {
         int local = 0;
         for (int w = 0; w < nw; ++w) local += sh_warp_cnt[w];
         const unsigned long long ep = static_cast<unsigned long long>(static_cast<unsigned>(epoch)) << 32;
@@ -171,8 +187,8 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
     for (int w = 0; w < wid; ++w) rank += sh_warp_cnt[w];
     rank += __popc(pop_mask & ((1u << (lane & ~1)) - 1u));
     const int top = sh_pop_base;
-    if (pop && rank == top && q == 0) set_status(s.status, PE_POOL_EXHAUSTED);  // first failing pop
-    const bool served = live && (pop ? rank < top : rank <= top);
+    if (!fast && pop && rank == top && q == 0) set_status(s.status, PE_POOL_EXHAUSTED);  // first failing pop
+    const bool served = live && (pop ? !fast && rank < top : rank <= top);
 
     int page = 0;
     if (served) {
@@ -229,6 +245,11 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
             s.page_scores[page] = sum / static_cast<double>(cnt);
         }
     }
+    // will this table pop on the next append? (its newest page is now full;
+    // an unserved table is flagged conservatively)
+    const bool next_pop = has && q == 0 && (served ? slot + 1 == s.B : true);
+    if (__syncthreads_or(next_pop) && threadIdx.x == 0)
+        *reinterpret_cast<volatile unsigned int*>(&ctl->pop_flag) = static_cast<unsigned>(epoch % 0x3FFFFFFF + 1);
     (void)nw;
 }
 
@@ -428,9 +449,10 @@ void launch_evict_score(dim3 grid, int threads, cudaStream_t st, const DevState&
 template <int SV>
 void launch_append(int blocks, cudaStream_t st, const DevState& s, const TableSet& ts, const uint8_t* k,
                    const uint8_t* v, const int64_t* pos, unsigned long long* lb, unsigned long long* lbg,
-                   LaunchCtl* ctl,
+                   LaunchCtl* ctl, int fast_ok,
                    unsigned long long ticket_base, int epoch) {
-    append_kernel<SV><<<blocks, kAppendThreads, 0, st>>>(s, ts, k, v, pos, lb, lbg, ctl, ticket_base, epoch);
+    append_kernel<SV><<<blocks, kAppendThreads, 0, st>>>(s, ts, k, v, pos, lb, lbg, ctl, ticket_base, epoch,
+                                                           fast_ok);
 }
 
 void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st, const DevState& s,
@@ -443,8 +465,9 @@ void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st
 void launch_append_any(int variant, int blocks, cudaStream_t st, const DevState& s, const TableSet& ts,
                        const uint8_t* k, const uint8_t* v, const int64_t* pos, unsigned long long* lb,
                        unsigned long long* lbg,
-                       LaunchCtl* ctl, unsigned long long ticket_base, int epoch) {
-    PE_SCORE_DISPATCH(variant, (launch_append<SV>(blocks, st, s, ts, k, v, pos, lb, lbg, ctl, ticket_base, epoch)));
+                       LaunchCtl* ctl, unsigned long long ticket_base, int epoch, bool fast_ok) {
+    PE_SCORE_DISPATCH(variant, (launch_append<SV>(blocks, st, s, ts, k, v, pos, lb, lbg, ctl, fast_ok ? 1 : 0,
+                                                  ticket_base, epoch)));
 }
 
 // ---------------------------------------------------------------------------

@@ -71,6 +71,11 @@ struct pe_engine {
     int32_t* vpage = nullptr;           // per launch table released page id (or -1)
     unsigned long long* lb_status = nullptr;  // append look-back status words (one per CTA)
     int append_epoch = 0;
+    // K0 no-pop fast path: the previous engine operation was an all-table
+    // append over the same layer range (the device flag written by that
+    // launch then says whether any table will pop on this one)
+    bool append_chain = false;
+    int32_t chain_layer0 = -1, chain_layers = 0;
     unsigned long long grid_tickets = 0;  // host mirror of DevState::grid_ctr
     double* evict_scratch = nullptr;
     int32_t* tab_len = nullptr;
@@ -492,6 +497,7 @@ pe_status pe_engine_destroy(pe_engine* e) {
 pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, const void* v,
                                 const int32_t* cu_seqlens, int32_t seq_begin, int32_t n_seqs,
                                 int32_t* evicted_counts, void* stream) {
+    if (e != nullptr) e->append_chain = false;  // tables change outside the append chain
     if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
     const DevState& s = e->s;
     if (layer < 0 || layer >= s.n_layers) return fail(PE_INVALID_ARG, "layer out of range");
@@ -742,6 +748,7 @@ namespace {
 // copy with the table API's per-call budget).
 pe_status launch_evict(pe_engine* e, const DevState& sc, const TableSet& ts, int32_t mode, int32_t* victims,
                        cudaStream_t st) {
+    if (e != nullptr) e->append_chain = false;  // tables change outside the append chain
     const int n = ts.size(sc);
     const bool vic_dev = victims && is_device_ptr(victims);
     int32_t* vdst = vic_dev ? victims : e->victims;
@@ -791,9 +798,16 @@ pe_status launch_append(pe_engine* e, const TableSet& ts, const uint8_t* dk, con
     const unsigned long long ticket_base = e->grid_tickets;
     e->grid_tickets += blocks;
     e->append_epoch = (e->append_epoch % 0x3FFFFFFF) + 1;
+    const bool contiguous = ts.ids == nullptr;
+    const char* ff = std::getenv("PE_APPEND_FAST");
+    const bool fast_ok = contiguous && e->append_chain && e->chain_layer0 == ts.layer_begin &&
+                         e->chain_layers == ts.n_layers && !(ff != nullptr && std::strcmp(ff, "0") == 0);
     launch_append_any(e->variant, blocks, st, s, ts, dk, dv, dp, e->lb_status,
-                      e->lb_status + lb_cta_words(s.n_tables), e->ctl, ticket_base, e->append_epoch);
+                      e->lb_status + lb_cta_words(s.n_tables), e->ctl, ticket_base, e->append_epoch, fast_ok);
     mark_consumed(e, st);
+    e->append_chain = contiguous;
+    e->chain_layer0 = ts.layer_begin;
+    e->chain_layers = ts.n_layers;
     pe_status r = check_launch(e, "append_kernel");
     if (r != PE_OK) return r;
     e->stats.kernel_launches += 1;
@@ -1122,6 +1136,7 @@ pe_status pe_table_append(pe_engine* e, int32_t n, const int32_t* table_ids, con
 
 pe_status pe_table_evict(pe_engine* e, int32_t n, const int32_t* table_ids, int32_t cache_budget, int32_t mode,
                          int32_t* victims, void* stream) {
+    if (e != nullptr) e->append_chain = false;  // tables change outside the append chain
     pe_status r = check_table_list(e, n, table_ids);
     if (r != PE_OK) return r;
     if (cache_budget < 0) return fail(PE_BUDGET_INVALID, "negative budget");
@@ -1141,6 +1156,7 @@ pe_status pe_table_evict(pe_engine* e, int32_t n, const int32_t* table_ids, int3
 }
 
 pe_status pe_table_free_page(pe_engine* e, int32_t table, int32_t logical_index, void* stream) {
+    if (e != nullptr) e->append_chain = false;  // tables change outside the append chain
     pe_status r = check_table(e, table);
     if (r != PE_OK) return r;
     cudaSetDevice(e->device);
@@ -1150,6 +1166,7 @@ pe_status pe_table_free_page(pe_engine* e, int32_t table, int32_t logical_index,
 }
 
 pe_status pe_table_clear(pe_engine* e, int32_t table, void* stream) {
+    if (e != nullptr) e->append_chain = false;  // tables change outside the append chain
     pe_status r = check_table(e, table);
     if (r != PE_OK) return r;
     cudaSetDevice(e->device);
@@ -1215,6 +1232,7 @@ pe_status pe_read_table(pe_engine* e, int32_t table, int32_t* page_ids, int32_t*
 
 pe_status pe_table_evict_token(pe_engine* e, int32_t table, int32_t rule, int64_t arg, int32_t cache_budget,
                                int64_t newest_position, int64_t* victim_position, void* stream) {
+    if (e != nullptr) e->append_chain = false;  // tables change outside the append chain
     pe_status r = check_table(e, table);
     if (r != PE_OK) return r;
     if (rule < PE_TOKEN_AT_POSITION || rule > PE_TOKEN_KEY_DIFF) return fail(PE_INVALID_ARG, "token rule");
@@ -1235,6 +1253,7 @@ pe_status pe_table_evict_token(pe_engine* e, int32_t table, int32_t rule, int64_
 
 pe_status pe_decode_evict_tokens(pe_engine* e, int32_t layer_begin, int32_t n_layers, int32_t rule, int64_t arg,
                                  const int64_t* newest_positions, int64_t* victim_positions, void* stream) {
+    if (e != nullptr) e->append_chain = false;  // tables change outside the append chain
     if (e == nullptr || newest_positions == nullptr) return fail(PE_INVALID_ARG, "null argument");
     DevState& s = e->s;
     if (layer_begin < 0 || n_layers <= 0 || layer_begin + n_layers > s.n_layers)
@@ -1325,6 +1344,7 @@ pe_status pe_check_invariants(pe_engine* e, pe_invariants* out) {
 }
 
 pe_status pe_pool_allocate(pe_engine* e, int32_t* page_id) {
+    if (e != nullptr) e->append_chain = false;  // tables change outside the append chain
     if (e == nullptr || page_id == nullptr) return fail(PE_INVALID_ARG, "null argument");
     cudaSetDevice(e->device);
     pool_allocate_kernel<<<1, 1>>>(e->s, e->alloc_out);
@@ -1337,6 +1357,7 @@ pe_status pe_pool_allocate(pe_engine* e, int32_t* page_id) {
 }
 
 pe_status pe_pool_release(pe_engine* e, int32_t page_id) {
+    if (e != nullptr) e->append_chain = false;  // tables change outside the append chain
     if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
     if (page_id < 0 || page_id >= e->s.capacity) return fail(PE_INDEX_OUT_OF_RANGE, "page id out of range");
     cudaSetDevice(e->device);

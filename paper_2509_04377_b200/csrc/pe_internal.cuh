@@ -62,6 +62,7 @@ struct LaunchCtl {
     int32_t ready;      // unused (kept for layout)
     int32_t pad_;
     unsigned long long top_word;  // append look-back: epoch << 32 | stack top before the launch's pops
+    unsigned int pop_flag;        // = epoch E: some table pops (or may pop) at append launch E
 };
 
 // Launch table set: decode launches cover every sequence for layers

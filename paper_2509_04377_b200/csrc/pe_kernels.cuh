@@ -54,7 +54,7 @@ const void* prefill_fused_fn(int variant);
 void launch_append_any(int variant, int blocks, cudaStream_t st, const DevState& s, const TableSet& ts,
                        const uint8_t* k, const uint8_t* v, const int64_t* pos, unsigned long long* lb,
                        unsigned long long* lbg,
-                       LaunchCtl* ctl, unsigned long long ticket_base, int epoch);
+                       LaunchCtl* ctl, unsigned long long ticket_base, int epoch, bool fast_ok);
 void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st, const DevState& s,
                             const TableSet& ts, int ppc, double* scratch, int32_t* tickets, int32_t* vpage,
                             int32_t* victims, unsigned long long grid_last);

@@ -157,6 +157,47 @@ def test_decode_parity(dtype, mode):
     assert eng.stats().pages_evicted > 0
 
 
+@pytest.mark.parametrize("fast", ["1", "0"])
+def test_append_chain_parity(fast, monkeypatch):
+    """Runs of consecutive appends (the K0 no-pop fast path: the previous
+    append over the same layer range flagged no popping table), broken by
+    evictions and per-layer appends (a range change); an initially empty
+    layer and mixed lengths so pops happen at different steps
+    in different tables. Bit-exact against the oracle after every launch;
+    PE_APPEND_FAST=0 runs the same schedule through the look-back only."""
+    monkeypatch.setenv("PE_APPEND_FAST", fast)
+    rng = np.random.default_rng(77)
+    B, C, H, n_layers, S, d = 8, 32, 2, 3, 4, 64
+    lens = np.array([C + 3, 7, 2 * C, 1])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    # evictions every B steps only: tables may hold up to C + 2B tokens
+    eng, orc = make_pair(n_seqs=S, n_layers=n_layers, H=H, d=d, B=B, C=C, dtype=oracle.F32,
+                         max_pages=C // B + 4)
+    for layer in range(n_layers - 1):  # the last layer starts empty (its first append pops)
+        k, _ = random_kv(rng, (cu[-1], H, d), oracle.F32)
+        v, _ = random_kv(rng, (cu[-1], H, d), oracle.F32)
+        eng.prefill_compress(layer, dev(k), dev(v), cu)
+        orc.prefill(layer, k, v, cu)
+    pos = lens.astype(np.int64).copy()
+    for step in range(1, 4 * B + 3):
+        k, _ = random_kv(rng, (n_layers, S, H, d), oracle.F32)
+        v, _ = random_kv(rng, (n_layers, S, H, d), oracle.F32)
+        if step % 11 == 5:  # per-layer appends (range change breaks the chain)
+            for layer in range(n_layers):
+                eng.append_token(layer, 1, dev(k[layer:layer + 1]), dev(v[layer:layer + 1]), dev(pos))
+                assert orc.decode_append(layer, 1, k[layer:layer + 1], v[layer:layer + 1], pos) == 0
+        else:
+            eng.append_token(0, n_layers, dev(k), dev(v), dev(pos))
+            assert orc.decode_append(0, n_layers, k, v, pos) == 0
+        if step % B == 0:
+            vic = eng.evict(0, n_layers, step=step, victims=True)
+            _, ovic = orc.decode_evict(0, n_layers)
+            np.testing.assert_array_equal(vic, ovic, err_msg=f"step {step}")
+        pos += 1
+        eng.sync()
+        check(eng, orc, f"step {step}: ", pages=(step % 8 == 0))
+
+
 def test_engine_matches_compiled_reference(reference):
     """Direct replay through the reference's own PagePool/BlockTable/policy."""
     rng = np.random.default_rng(42)
