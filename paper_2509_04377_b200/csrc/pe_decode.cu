@@ -367,7 +367,7 @@ __device__ __forceinline__ int publish_chunk(const DevState& s, int t, int y, in
 // The last CTA of the table (atomic ticket) takes the argmin and evicts; the
 // last CTA of the grid pushes the released pages.
 template <int SV, bool HOLES>
-__global__ void __launch_bounds__(kEvictThreads, 4) evict_score_kernel(
+__global__ void __launch_bounds__(kEvictThreads, 5) evict_score_kernel(
     DevState s, TableSet ts, int pages_per_cta, double* scratch, int32_t* tickets, int32_t* vpage,
     int32_t* victims, unsigned long long grid_last) {
     __shared__ double page_mean[kMaxPagesPerCta];
