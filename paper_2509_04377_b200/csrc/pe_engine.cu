@@ -418,6 +418,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             !allow(attention_mma_fn(64), &mma64) || !allow(attention_mma_fn(128), &mma128) ||
             !allow(reinterpret_cast<const void*>(prefill_select_cta_kernel), &sel_cta) ||
             !allow(reinterpret_cast<const void*>(prefill_select_stream_kernel), &sel_cta) ||
+            !allow(reinterpret_cast<const void*>(prefill_select_stream512_kernel), &sel_cta) ||
             !allow(prefill_fused_fn(e->variant), &sel_cta)) {
             cudaGetLastError();
             return cleanup_fail(fail(PE_CUDA_ERROR, "cudaFuncSetAttribute(max dynamic smem) failed"));
@@ -575,25 +576,31 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     a.layer = layer;
     a.score_tokens = kScoreTokensPerCta;
     // PE_SELECT=cluster forces the cluster kernel (tests exercise both paths)
+    // Select kernels. Default: tables of up to kSelectCtaMaxLen tokens take the
+    // 512-thread streamed CTA select (two CTAs per SM), longer ones the
+    // 1024-thread streamed select with a 16K candidate list. A/B options:
+    // PE_SELECT=smem (short tables: high words in shared memory, the previous
+    // default), PE_SELECT=stream (every table: the 1024-thread streamed
+    // select), PE_SELECT=cluster (every table: the 8-CTA cluster select),
+    // PE_SELECT_LONG=cluster (long tables: the cluster select),
+    // PE_SELECT_MIXED=0 (a call with long tables sends every table to the
+    // long-table kernel).
     const char* sel_env = std::getenv("PE_SELECT");
-    const bool force_cluster = sel_env != nullptr && std::strcmp(sel_env, "cluster") == 0;
-    const bool force_stream = sel_env != nullptr && std::strcmp(sel_env, "stream") == 0;  // A/B: every table streamed
-    if (force_stream) max_short = 0;
-    const bool use_cta_select = max_len <= kSelectCtaMaxLen && !force_cluster && !force_stream;
-    a.chunk_cap = use_cta_select ? max_len : chunk_cap;  // keys held in smem per CTA
+    auto env_is = [](const char* v, const char* x) { return v != nullptr && std::strcmp(v, x) == 0; };
+    const bool force_cluster = env_is(sel_env, "cluster");
+    const bool force_stream = env_is(sel_env, "stream");
+    const bool smem_short = env_is(sel_env, "smem");
+    const bool has_long = max_len > kSelectCtaMaxLen;
+    if (force_stream || force_cluster || (has_long && env_is(std::getenv("PE_SELECT_MIXED"), "0"))) max_short = 0;
+    const bool long_cluster = force_cluster || env_is(std::getenv("PE_SELECT_LONG"), "cluster");
+    const bool any_long = max_short == 0 || has_long;  // some table goes to the long-table kernel
+    // the shared-memory select (and the fused variant built on it) holds a
+    // whole table's high words per CTA; the cluster select a chunk per CTA
+    const bool smem_capable = !has_long && !force_cluster && !force_stream;
+    a.chunk_cap = smem_capable ? max_len : chunk_cap;
     a.cta_len_max = 0x7FFFFFFF;
     a.cluster_len_min = -1;
-    // Mixed lengths with some tables too long for the CTA select: the short
-    // tables still take the CTA select, only the long ones the cluster select
-    // (each kernel skips the other's tables). PE_SELECT_MIXED=0 disables it.
-    const char* mx = std::getenv("PE_SELECT_MIXED");
-    const bool mixed_select = !use_cta_select && !force_cluster && max_short > 0 &&
-                              !(mx != nullptr && std::strcmp(mx, "0") == 0);
-    // Tables over the limit take the CTA select with its high words streamed
-    // from global memory (one CTA per table); PE_SELECT_LONG=cluster keeps the
-    // 8-CTA cluster select for them.
-    const char* lg = std::getenv("PE_SELECT_LONG");
-    const bool stream_long = !use_cta_select && !force_cluster && !(lg != nullptr && std::strcmp(lg, "cluster") == 0);
+    a.cand_cap = kSelCandCapStream;
     if (total_pages > INT32_MAX) return fail(PE_POOL_EXHAUSTED, "page pool exhausted");
     plan_prefill_kernel<<<1, 1024, 0, st>>>(s, a, static_cast<int32_t>(total_pages), e->ctl);
     // Opt-in (PE_PREFILL_FUSED=1): the persistent single-launch variant. On
@@ -601,7 +608,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     // multi-kernel wave pipeline below (its 1024-thread CTAs keep fewer
     // loads in flight while scoring), so the wave pipeline is the default.
     const char* fz = std::getenv("PE_PREFILL_FUSED");
-    if (use_cta_select && fz != nullptr && std::strcmp(fz, "1") == 0) {
+    if (smem_capable && fz != nullptr && std::strcmp(fz, "1") == 0) {
         // one persistent launch: score units and per-table select+copy items,
         // X(q) scheduled after S(q+1) (prefill_fused_kernel)
         int kUnitTokens = 1024;
@@ -664,9 +671,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     // The canonical page reservation (plan) is made once for the whole call.
     // (the cluster select of long tables is kept out of the wave overlap: its
     // 8-CTA clusters co-schedule badly next to another stream's kernels)
-    const char* lw = std::getenv("PE_LONG_WAVES");  // sequence waves with the streamed long-table select
-    const bool long_waves = stream_long && lw != nullptr && std::strcmp(lw, "1") == 0;
-    int waves = (!use_cta_select && !long_waves) ? 1 : (n_seqs >= 2 ? 2 : 1);
+    int waves = (any_long && long_cluster) ? 1 : (n_seqs >= 2 ? 2 : 1);
     if (const char* wv = std::getenv("PE_PREFILL_WAVES")) waves = std::max(1, std::min(n_seqs, std::atoi(wv)));
     if (waves > 1) {
         PE_CUDA(cudaEventRecord(e->ev_fork, st));
@@ -688,41 +693,35 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
         aw.n_tab = (q1 - q0) * H;
         launch_prefill_score_any(e->variant, dim3((max_len + aw.score_tokens - 1) / aw.score_tokens, q1 - q0),
                                  sw, s, aw, e->ctl);
-        if (use_cta_select) {
-            // one CTA per table, high key words in shared memory (no cluster barriers)
-            const size_t sel_smem =
-                (((size_t)max_len * 4 + 15) & ~size_t(15)) + kSelHistCopies * 2048 * 4 + kSelCandCap * 4;
-            prefill_select_cta_kernel<<<aw.n_tab, 1024, sel_smem, sw>>>(s, aw, e->ctl);
-        } else if (stream_long) {
-            if (max_short > 0) {  // tables <= kSelectCtaMaxLen: hi words in shared memory
-                PrefillArgs ac = aw;
+        if (max_short > 0) {  // tables of at most kSelectCtaMaxLen tokens
+            PrefillArgs ac = aw;
+            ac.cta_len_max = kSelectCtaMaxLen;
+            if (smem_short) {
                 ac.chunk_cap = max_short;
-                ac.cta_len_max = kSelectCtaMaxLen;
                 const size_t sel_smem =
                     (((size_t)max_short * 4 + 15) & ~size_t(15)) + kSelHistCopies * 2048 * 4 + kSelCandCap * 4;
                 prefill_select_cta_kernel<<<aw.n_tab, 1024, sel_smem, sw>>>(s, ac, e->ctl);
-                e->stats.kernel_launches += 1;
+            } else {
+                ac.cand_cap = kSelCandCap;
+                const size_t smem5 = (size_t)kSelHistCopies * 2048 * 4 + (size_t)kSelCandCap * 4;
+                prefill_select_stream512_kernel<<<aw.n_tab, 512, smem5, sw>>>(s, ac, e->ctl);
             }
+            e->stats.kernel_launches += 1;
+        }
+        if (any_long) {  // the longer tables (every table when max_short == 0)
             PrefillArgs al = aw;
             al.cluster_len_min = max_short > 0 ? kSelectCtaMaxLen : -1;
-            const size_t st_smem = (size_t)kSelHistCopies * 2048 * 4 + (size_t)kSelCandCapStream * 4;
-            prefill_select_stream_kernel<<<aw.n_tab, 1024, st_smem, sw>>>(s, al, e->ctl);
-        } else if (mixed_select) {
-            PrefillArgs ac = aw;  // tables <= kSelectCtaMaxLen
-            ac.chunk_cap = max_short;
-            ac.cta_len_max = kSelectCtaMaxLen;
-            const size_t sel_smem =
-                (((size_t)max_short * 4 + 15) & ~size_t(15)) + kSelHistCopies * 2048 * 4 + kSelCandCap * 4;
-            prefill_select_cta_kernel<<<aw.n_tab, 1024, sel_smem, sw>>>(s, ac, e->ctl);
-            PrefillArgs al = aw;  // the longer tables
-            al.cluster_len_min = kSelectCtaMaxLen;
-            prefill_select_kernel<<<dim3(kPrefillCluster, aw.n_tab), kPackThreads, pack_smem, sw>>>(s, al, e->ctl);
+            if (long_cluster) {
+                prefill_select_kernel<<<dim3(kPrefillCluster, aw.n_tab), kPackThreads, pack_smem, sw>>>(s, al,
+                                                                                                     e->ctl);
+            } else {
+                const size_t st_smem = (size_t)kSelHistCopies * 2048 * 4 + (size_t)kSelCandCapStream * 4;
+                prefill_select_stream_kernel<<<aw.n_tab, 1024, st_smem, sw>>>(s, al, e->ctl);
+            }
             e->stats.kernel_launches += 1;
-        } else {
-            prefill_select_kernel<<<dim3(kPrefillCluster, aw.n_tab), kPackThreads, pack_smem, sw>>>(s, aw, e->ctl);
         }
         prefill_copy_kernel<<<dim3((max_keep_pages + 3) / 4, aw.n_tab), 128, 0, sw>>>(s, aw, e->ctl);
-        e->stats.kernel_launches += 3;
+        e->stats.kernel_launches += 2;  // score + copy (the selects counted above)
     }
     if (waves > 1) {
         PE_CUDA(cudaEventRecord(e->ev_join, e->aux_stream));

@@ -31,6 +31,7 @@ struct PrefillArgs {
     int32_t score_tokens;                // tokens (x all heads) per score CTA
     int32_t cta_len_max;                 // CTA select: tables longer than this are skipped
     int32_t cluster_len_min;             // cluster select: tables this short or shorter are skipped
+    int32_t cand_cap;                    // streamed select: candidate list capacity (shared memory)
 };
 
 __global__ void evict_cached_kernel(DevState s, TableSet ts, double* scratch, int32_t* vpage, int32_t* victims,
@@ -43,6 +44,7 @@ constexpr int kSelCandCap = 4096;        // boundary-bin candidates compacted af
 constexpr int kSelectCtaMaxLen = 34816;  // CTA-per-table select: 4 B of smem per token + 64 KB histograms + 16 KB candidates
 constexpr int kSelCandCapStream = 16384;  // candidates of the streamed CTA select (no hi words in smem)
 __global__ void prefill_select_stream_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
+__global__ void prefill_select_stream512_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 __global__ void prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 // persistent fused prefill (score units + per-table select/copy), pe_prefill.cu
 void launch_prefill_fused_any(int variant, int grid, size_t smem, cudaStream_t st, const DevState& s,

@@ -500,7 +500,7 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
     const int t = (seq * s.n_layers + a.layer) * s.tab_heads + h;
     const int B = s.B;
     uint32_t* hi = reinterpret_cast<uint32_t*>(smem);  // SMEM_HI only
-    const int cand_cap = SMEM_HI ? kSelCandCap : kSelCandCapStream;
+    const int cand_cap = SMEM_HI ? kSelCandCap : a.cand_cap;
     // kSelHistCopies private histograms (warp w -> copy w % kSelHistCopies):
     // the early digits of a table's keys are concentrated in a few bins, so a
     // single histogram would serialise every warp's atomics on them
@@ -820,7 +820,20 @@ __global__ void __launch_bounds__(1024, 1) prefill_select_stream_kernel(DevState
                                                                         const LaunchCtl* ctl) {
     extern __shared__ __align__(16) uint8_t smem[];
     if (ctl->abort) return;
-    if (a.tab_len[blockIdx.x] <= a.cluster_len_min) return;
+    const int L = a.tab_len[blockIdx.x];
+    if (L <= a.cluster_len_min || L > a.cta_len_max) return;  // the other select kernel's table
+    select_table_cta<false>(s, a, blockIdx.x, smem, ctl);
+}
+
+// The streamed select with 512 threads and a 4096-entry candidate list: 80 KB
+// of shared memory and 32K registers, so two CTAs share an SM (A/B variant,
+// PE_SELECT=stream512).
+__global__ void __launch_bounds__(512, 2) prefill_select_stream512_kernel(DevState s, PrefillArgs a,
+                                                                          const LaunchCtl* ctl) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    if (ctl->abort) return;
+    const int L = a.tab_len[blockIdx.x];
+    if (L <= a.cluster_len_min || L > a.cta_len_max) return;  // the other select kernel's table
     select_table_cta<false>(s, a, blockIdx.x, smem, ctl);
 }
 

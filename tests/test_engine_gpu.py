@@ -48,10 +48,15 @@ def check(eng, orc, what="", pages=True):
                 assert st["page_scores"][pid] == ost["page_scores"][pid], f"{what}page score {pid}"
 
 
-@pytest.fixture(params=["cta", "cluster"])
+@pytest.fixture(params=["default", "smem", "stream", "cluster"])
 def select_path(request, monkeypatch):
-    """Run prefill through both select kernels (CTA-per-table and cluster)."""
-    monkeypatch.setenv("PE_SELECT", request.param)
+    """Run prefill through every select kernel: the default 512-thread
+    streamed CTA select, the shared-memory CTA select, the 1024-thread
+    streamed select and the 8-CTA cluster select."""
+    if request.param == "default":
+        monkeypatch.delenv("PE_SELECT", raising=False)
+    else:
+        monkeypatch.setenv("PE_SELECT", request.param)
     return request.param
 
 
@@ -97,11 +102,16 @@ def prefill_variant(request, monkeypatch):
     return request.param
 
 
+@pytest.mark.parametrize("sel", ["default", "smem"])
 @pytest.mark.parametrize("gen", [random_kv, grid_kv])
-def test_prefill_long_tables_windowed_select(gen, prefill_variant):
+def test_prefill_long_tables_windowed_select(gen, prefill_variant, sel, monkeypatch):
     """Tables of >= 8192 tokens take the sampled pivot window of the CTA
     select kernel (candidates only; tie-heavy grid data overflows the window
     and exercises the full-pass fallback). Bit-exact against the oracle."""
+    if sel == "smem":
+        monkeypatch.setenv("PE_SELECT", "smem")
+    else:
+        monkeypatch.delenv("PE_SELECT", raising=False)
     rng = np.random.default_rng(8192)
     B, C, d, H = 16, 2048, 128, 2
     lens = np.array([8192, 32768, 20001, 9000, 4096 + 1])
