@@ -2,7 +2,7 @@
  * pe.h — C-ABI of the B200-native PagedEviction engine (libpe_b200.so).
  *
  * This is the drop-in boundary for the reference's C++ cache-manager API
- * (/root/reference/proj/core/include/pagedevict/*.hpp). One engine owns, in
+ * (/root/reference/proj/core/include/pagedevict/<header>.hpp). One engine owns, in
  * HBM of one GPU: the paged KV pool (PagePool), every table's block table
  * (BlockTable), the LIFO free list, the eviction policy and its budget
  * config (PolicyConfig). All compute runs in hand-written sm_100a kernels;
