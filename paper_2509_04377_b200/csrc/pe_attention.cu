@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_tma_kernel(DevState
     constexpr int NST = 3;
     constexpr int KS = D / 16;
     constexpr int NT = D / 8;
-    extern __shared__ __align__(1024) uint8_t smem[];
+    extern __shared__ __align__(16) uint8_t smem[];  // aligned to 1024 B by hand (align1024)
     __shared__ __align__(8) uint64_t bars[kAttnThreads / 32][NST];
     __shared__ int32_t ids[kAttnMaxSplitPages];
     const int lane = threadIdx.x & 31;
