@@ -575,6 +575,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     a.seq_begin = seq_begin;
     a.layer = layer;
     a.score_tokens = kScoreTokensPerCta;
+    if (const char* stk = std::getenv("PE_SCORE_TOKENS")) a.score_tokens = std::max(16, std::atoi(stk));  // tuning
     // PE_SELECT=cluster forces the cluster kernel (tests exercise both paths)
     // Select kernels. Default: tables of up to kSelectCtaMaxLen tokens take the
     // 512-thread streamed CTA select (two CTAs per SM), longer ones the
