@@ -47,7 +47,7 @@ __device__ __forceinline__ void merge_if_last(const DevState& s, const AttnArgs&
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    const int H = s.tab_heads;
+    const int H = a.kv_heads;
     const int h = i % H;
     const int seq = i / H;
     const int G = a.G;
@@ -73,19 +73,22 @@ __global__ void __launch_bounds__(kAttnThreads) attention_split_kernel(DevState 
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
-    const int i = blockIdx.y;            // launch table: seq * H + h
-    const int sp = blockIdx.x;           // split
-    const int H = s.tab_heads;
+    const int i = blockIdx.x;            // launch item: seq * kv_heads + h
+    const int sp = blockIdx.y;           // split
+    const int H = a.kv_heads;
     const int h = i % H;
     const int seq = i / H;
-    const int t = (seq * s.n_layers + a.layer) * H + h;
+    const int t = a.table(s, i);
     const int G = a.G;
-    const int d = s.w;
+    const int d = a.d;
     const int B = s.B;
     const int N = s.num_pages[t];
     const int p_begin = sp * a.pages_per_split;
     const int p_end = min(N, p_begin + a.pages_per_split);
-    const int row_pitch = s.row_bytes + 16;
+    const int elt = s.dtype == PE_DTYPE_BF16 ? 2 : 4;
+    const int head_bytes = d * elt;       // this head's slice of each row
+    const int col = a.col_elems(i) * elt;
+    const int row_pitch = head_bytes + 16;
     const int stage_bytes = 2 * B * row_pitch;
 
     // shared layout: q [G][d] float | p [nw][G][16] float | warp partials | stages
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_split_kernel(DevState 
     for (int x = threadIdx.x; x < G * d; x += blockDim.x) {
         const int g = x / d;
         const int dd = x % d;
-        const uint8_t* qrow = a.q + ((int64_t)seq * a.n_q_heads + h * G + g) * s.row_bytes;
+        const uint8_t* qrow = a.q + ((int64_t)seq * a.n_q_heads + h * G + g) * head_bytes;
         q_sm[x] = elem_f32(qrow, dd, s.dtype) * a.scale_log2;
     }
     __syncthreads();
@@ -119,11 +122,11 @@ __global__ void __launch_bounds__(kAttnThreads) attention_split_kernel(DevState 
 
     const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
     const int my_n = (p_end - p_begin) > wid ? ((p_end - p_begin) - wid + nw - 1) / nw : 0;
-    const int pieces = s.row_bytes / 16;
+    const int pieces = head_bytes / 16;
     auto issue = [&](int k) {
         if (k < my_n) {
             const int pg = p_begin + wid + k * nw;
-            const uint8_t* base = s.pages + (int64_t)row[pg] * 2 * B * s.pitch;
+            const uint8_t* base = s.pages + (int64_t)row[pg] * 2 * B * s.pitch + col;
             const int fill = (pg == N - 1) ? s.newest_fill[t] : B;
             uint8_t* st = my_stage + (k % kAttnStages) * stage_bytes;
             const int total = 2 * B * pieces;
@@ -340,12 +343,13 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_mma_kernel(DevState
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
-    const int i = blockIdx.y;
-    const int sp = blockIdx.x;
-    const int H = s.tab_heads;
+    const int i = blockIdx.x;
+    const int sp = blockIdx.y;
+    const int H = a.kv_heads;
     const int h = i % H;
     const int seq = i / H;
-    const int t = (seq * s.n_layers + a.layer) * H + h;
+    const int t = a.table(s, i);
+    const int col = a.col_elems(i) * 2;
     const int G = a.G;
     const int N = s.num_pages[t];
     const int p_begin = sp * a.pages_per_split;
@@ -385,13 +389,13 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_mma_kernel(DevState
         if (k < my_n) {
             const int pg = p_begin + wid + k * nw;
             const int32_t id = ids_sm ? ids[pg - p_begin] : __ldg(row + pg);
-            const uint8_t* base = s.pages + (int64_t)id * 32 * RB;
+            const uint8_t* base = s.pages + (int64_t)id * 32 * s.pitch + col;
             uint8_t* st = stage + (k % NST) * PAGE_SM;
 #pragma unroll
             for (int x = lane; x < 32 * PIECES; x += 32) {
                 const int r = x / PIECES;
                 const int pc = x - r * PIECES;
-                cp_async16(st + r * RP + pc * 16, base + r * RB + pc * 16);
+                cp_async16(st + r * RP + pc * 16, base + (int64_t)r * s.pitch + pc * 16);
             }
         }
         cp_async_commit();
@@ -550,12 +554,13 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_tma_kernel(DevState
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
-    const int i = blockIdx.y;
-    const int sp = blockIdx.x;
-    const int H = s.tab_heads;
+    const int i = blockIdx.x;
+    const int sp = blockIdx.y;
+    const int H = a.kv_heads;
     const int h = i % H;
     const int seq = i / H;
-    const int t = (seq * s.n_layers + a.layer) * H + h;
+    const int t = a.table(s, i);
+    const int col = a.col_elems(i);  // tensor-map column of this head's slice
     const int G = a.G;
     const int N = s.num_pages[t];
     const int p_begin = sp * a.pages_per_split;
@@ -593,7 +598,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_tma_kernel(DevState
         if (k < my_n && lane == 0) {
             const int pg = p_begin + wid + k * nw;
             const int32_t id = ids_sm ? ids[pg - p_begin] : __ldg(row + pg);
-            tma_load_page(smem_u32(stage + (k % NST) * PAGE_SM), &bars[wid][k % NST], &tmap, id * 32, HALVES,
+            tma_load_page(smem_u32(stage + (k % NST) * PAGE_SM), &bars[wid][k % NST], &tmap, id * 32, col, HALVES,
                           PAGE_SM);
         }
     };

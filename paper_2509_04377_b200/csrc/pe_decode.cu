@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
         // no-pop fast path: the previous append over the same tables (and no
         // other table operation since, fast_ok) flagged no table as popping
         // on this launch, so every pop rank is 0 and the look-back is skipped
-        sh_fast = fast_ok && *reinterpret_cast<volatile unsigned int*>(&ctl->pop_flag) != static_cast<unsigned>(epoch);
+        sh_fast = fast_ok &&
+                  *reinterpret_cast<volatile unsigned int*>(&ctl->pop_flag[epoch & 1]) != static_cast<unsigned>(epoch);
     }
     __syncthreads();
     PE_TR(1);
@@ -248,8 +249,10 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
     // will this table pop on the next append? (its newest page is now full;
     // an unserved table is flagged conservatively)
     const bool next_pop = has && q == 0 && (served ? slot + 1 == s.B : true);
-    if (__syncthreads_or(next_pop) && threadIdx.x == 0)
-        *reinterpret_cast<volatile unsigned int*>(&ctl->pop_flag) = static_cast<unsigned>(epoch % 0x3FFFFFFF + 1);
+    if (__syncthreads_or(next_pop) && threadIdx.x == 0) {
+        const int next = epoch % kAppendEpochPeriod + 1;  // the next launch's epoch (opposite parity)
+        *reinterpret_cast<volatile unsigned int*>(&ctl->pop_flag[next & 1]) = static_cast<unsigned>(next);
+    }
     (void)nw;
 }
 

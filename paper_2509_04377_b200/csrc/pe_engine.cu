@@ -324,6 +324,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         return st;
     };
     const size_t page_bytes = (size_t)2 * s.B * s.pitch;
+    const size_t attn_items = std::max<size_t>((size_t)n_tables, (size_t)c.n_seqs * c.n_kv_heads);
     if (cudaMalloc(&s.pages, (size_t)cap * page_bytes) != cudaSuccess ||
         dalloc(&s.positions, (size_t)cap * s.B) != cudaSuccess ||
         dalloc(&s.token_scores, (size_t)cap * s.B) != cudaSuccess ||
@@ -336,7 +337,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         dalloc(&s.holes, (size_t)cap) != cudaSuccess ||
         dalloc(&e->vpage, n_tables) != cudaSuccess || dalloc(&e->ctl, 1) != cudaSuccess ||
         dalloc(&e->alloc_out, 1) != cudaSuccess || dalloc(&e->tok_out, 1) != cudaSuccess ||
-        dalloc(&e->attn_tickets, n_tables) != cudaSuccess ||
+        dalloc(&e->attn_tickets, attn_items) != cudaSuccess ||
         dalloc(&e->seq_units, c.n_seqs) != cudaSuccess || dalloc(&e->seq_done, c.n_seqs) != cudaSuccess ||
         dalloc(&e->work_ctr, 1) != cudaSuccess ||
         dalloc(&e->lb_status, lb_words(n_tables)) != cudaSuccess ||
@@ -375,7 +376,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             cudaMemset(s.evict_count, 0, sizeof(unsigned long long)) != cudaSuccess ||
             cudaMemset(s.grid_ctr, 0, sizeof(unsigned long long)) != cudaSuccess ||
             cudaMemset(e->tickets, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
-            cudaMemset(e->attn_tickets, 0, sizeof(int32_t) * n_tables) != cudaSuccess ||
+            cudaMemset(e->attn_tickets, 0, sizeof(int32_t) * attn_items) != cudaSuccess ||
             cudaMemset(e->lb_status, 0, sizeof(unsigned long long) * lb_words(n_tables)) != cudaSuccess ||
             cudaMemset(e->ctl, 0, sizeof(LaunchCtl)) != cudaSuccess ||
             cudaMemset(e->victims, 0xFF, sizeof(int32_t) * n_tables) != cudaSuccess ||
@@ -425,7 +426,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         }
     }
     // tensor map over the pool for the TMA attention variant (bf16, d = 128, B = 16)
-    if (c.dtype == PE_DTYPE_BF16 && (s.w == 128 || s.w == 64) && s.B == 16) {
+    if (c.dtype == PE_DTYPE_BF16 && (c.head_dim == 128 || c.head_dim == 64) && s.B == 16) {
         using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                                          CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -447,9 +448,9 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         cudaFuncAttributes fa{};
         int optin = 0;
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device);
-        if (cudaFuncGetAttributes(&fa, attention_tma_fn(s.w)) == cudaSuccess) {
+        if (cudaFuncGetAttributes(&fa, attention_tma_fn(c.head_dim)) == cudaSuccess) {
             tma_smem = optin - static_cast<int>(fa.sharedSizeBytes);
-            cudaFuncSetAttribute(attention_tma_fn(s.w), cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem);
+            cudaFuncSetAttribute(attention_tma_fn(c.head_dim), cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem);
         }
         cudaGetLastError();
     }
@@ -674,6 +675,10 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     // 8-CTA clusters co-schedule badly next to another stream's kernels)
     int waves = (any_long && long_cluster) ? 1 : (n_seqs >= 2 ? 2 : 1);
     if (const char* wv = std::getenv("PE_PREFILL_WAVES")) waves = std::max(1, std::min(n_seqs, std::atoi(wv)));
+    // grid limits: the score grid's y (sequences of a wave) and the cluster
+    // select's y (tables of a wave) are at most 65535
+    waves = std::max(waves, (n_seqs + 65534) / 65535);
+    if (any_long && long_cluster) waves = std::max(waves, (n_tab + 65534) / 65535);
     if (waves > 1) {
         PE_CUDA(cudaEventRecord(e->ev_fork, st));
         PE_CUDA(cudaStreamWaitEvent(e->aux_stream, e->ev_fork, 0));
@@ -721,7 +726,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
             }
             e->stats.kernel_launches += 1;
         }
-        prefill_copy_kernel<<<dim3((max_keep_pages + 3) / 4, aw.n_tab), 128, 0, sw>>>(s, aw, e->ctl);
+        prefill_copy_kernel<<<dim3(aw.n_tab, (max_keep_pages + 3) / 4), 128, 0, sw>>>(s, aw, e->ctl);
         e->stats.kernel_launches += 2;  // score + copy (the selects counted above)
     }
     if (waves > 1) {
@@ -797,7 +802,7 @@ pe_status launch_append(pe_engine* e, const TableSet& ts, const uint8_t* dk, con
     const int blocks = (n + 16 * warps - 1) / (16 * warps);
     const unsigned long long ticket_base = e->grid_tickets;
     e->grid_tickets += blocks;
-    e->append_epoch = (e->append_epoch % 0x3FFFFFFF) + 1;
+    e->append_epoch = (e->append_epoch % kAppendEpochPeriod) + 1;  // 1 .. period, parity alternates
     const bool contiguous = ts.ids == nullptr;
     const char* ff = std::getenv("PE_APPEND_FAST");
     const bool fast_ok = contiguous && e->append_chain && e->chain_layer0 == ts.layer_begin &&
@@ -893,22 +898,27 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
                                     int32_t n_q_heads, void* stream) {
     if (e == nullptr) return fail(PE_INVALID_ARG, "null engine");
     const DevState& s = e->s;
-    if (e->cfg.granularity != PE_GRANULARITY_PER_KV_HEAD)
-        return fail(PE_INVALID_ARG, "attention requires PER_KV_HEAD tables");
     if (s.holes_on)
         return fail(PE_INVALID_STATE, "tables with evicted slots (unstructured eviction): use pe_table_attend");
     if (layer < 0 || layer >= s.n_layers) return fail(PE_INVALID_ARG, "layer out of range");
-    if (n_q_heads <= 0 || n_q_heads % s.tab_heads != 0)
+    // attention heads: the model's KV heads (a PER_LAYER table holds all of a
+    // layer's KV heads side by side in each row, kv_vector.hpp:23-27)
+    const int Hk = e->cfg.n_kv_heads;
+    const int hd = e->cfg.head_dim;
+    if (n_q_heads <= 0 || n_q_heads % Hk != 0)
         return fail(PE_LENGTH_MISMATCH, "query heads must be a multiple of KV heads");
-    const int G = n_q_heads / s.tab_heads;
+    const int G = n_q_heads / Hk;
     if (G > 8) return fail(PE_INVALID_ARG, "at most 8 query heads per KV head");
-    if (s.w > 256) return fail(PE_INVALID_ARG, "head_dim > 256 unsupported");
+    if (hd > 256) return fail(PE_INVALID_ARG, "head_dim > 256 unsupported");
+    if ((hd * (s.dtype == PE_DTYPE_BF16 ? 2 : 4)) % 16 != 0)
+        return fail(PE_INVALID_ARG, "head_dim * element size must be a multiple of 16 bytes");
     cudaSetDevice(e->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int n_tab = s.n_seqs * s.tab_heads;
+    const int n_tab = s.n_seqs * Hk;  // launch items (sequence, KV head)
+    const size_t head_bytes = (size_t)hd * (s.dtype == PE_DTYPE_BF16 ? 2 : 4);
     const uint8_t* dq = nullptr;
     e->n_pending = 0;
-    pe_status r = as_device(e, q, (size_t)s.n_seqs * n_q_heads * s.row_bytes, st, &dq);
+    pe_status r = as_device(e, q, (size_t)s.n_seqs * n_q_heads * head_bytes, st, &dq);
     if (r != PE_OK) return r;
     // as few splits as fill the GPU once (2 CTAs per SM): a CTA's warps stream
     // their pages without draining, so long CTAs beat extra waves (cfg3: one
@@ -918,12 +928,13 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
     splits = std::min(splits, std::max(1, (s.max_pages + 3) / 4));
     const int pps = (s.max_pages + splits - 1) / splits;
     splits = (s.max_pages + pps - 1) / pps;
-    r = ensure_t(&e->part_o, &e->part_o_elems, (size_t)n_tab * splits * G * s.w);
+    if (splits > 65535) return fail(PE_INVALID_ARG, "attention split count exceeds the grid limit");
+    r = ensure_t(&e->part_o, &e->part_o_elems, (size_t)n_tab * splits * G * hd);
     if (r != PE_OK) return r;
     r = ensure_t(&e->part_ml, &e->part_ml_elems, (size_t)n_tab * splits * G * 2);
     if (r != PE_OK) return r;
     const bool out_dev = is_device_ptr(out);
-    const size_t out_elems = (size_t)s.n_seqs * n_q_heads * s.w;
+    const size_t out_elems = (size_t)s.n_seqs * n_q_heads * hd;
     if (!out_dev) {
         r = ensure_t(&e->out_stage, &e->out_stage_elems, out_elems);
         if (r != PE_OK) return r;
@@ -939,24 +950,27 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
     a.n_q_heads = n_q_heads;
     a.splits = splits;
     a.pages_per_split = pps;
-    a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(s.w)));
-    const bool use_mma = s.dtype == PE_DTYPE_BF16 && s.B == 16 && (s.w == 64 || s.w == 128);
+    a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(hd)));
+    a.kv_heads = Hk;
+    a.heads_per_table = Hk / s.tab_heads;
+    a.d = hd;
+    const bool use_mma = s.dtype == PE_DTYPE_BF16 && s.B == 16 && (hd == 64 || hd == 128);
     // TMA staging (tensor map, 128-byte swizzle) unless PE_ATTN_TMA=0: 7 % faster
     // than the cp.async staging at cfg3 (160 vs 172 us), 11 % on the unpruned layer
     const char* tv = std::getenv("PE_ATTN_TMA");
     const bool use_tma = use_mma && e->has_tmap && !(tv != nullptr && std::strcmp(tv, "0") == 0);
     if (use_tma) {
-        launch_attention_tma(s.w, dim3(splits, n_tab), attention_tma_smem(s.w, G), st, s, a, &e->pool_tmap);
+        launch_attention_tma(hd, dim3(n_tab, splits), attention_tma_smem(hd, G), st, s, a, &e->pool_tmap);
     } else if (use_mma) {
         // tensor-core path (mma.sync bf16, P split hi/lo), pe_attention.cu
-        const size_t smem = attention_mma_smem(s.w, G);
-        launch_attention_mma(s.w, dim3(splits, n_tab), smem, st, s, a);
+        const size_t smem = attention_mma_smem(hd, G);
+        launch_attention_mma(hd, dim3(n_tab, splits), smem, st, s, a);
     } else {
         const int nw = 4;
-        size_t smem = (size_t)G * s.w * 4 + (size_t)nw * G * 16 * 4 + (size_t)nw * G * s.w * 4 +
-                      (size_t)nw * G * 2 * 4 + 16 + (size_t)nw * 2 * (2 * s.B * (s.row_bytes + 16));
+        size_t smem = (size_t)G * hd * 4 + (size_t)nw * G * 16 * 4 + (size_t)nw * G * hd * 4 +
+                      (size_t)nw * G * 2 * 4 + 16 + (size_t)nw * 2 * (2 * s.B * (head_bytes + 16));
         if (smem > (size_t)e->max_dyn_attn) return fail(PE_INVALID_ARG, "attention tile exceeds shared memory");
-        attention_split_kernel<<<dim3(splits, n_tab), 128, smem, st>>>(s, a);
+        attention_split_kernel<<<dim3(n_tab, splits), 128, smem, st>>>(s, a);
     }
     mark_consumed(e, st);
     r = check_launch(e, "attention");

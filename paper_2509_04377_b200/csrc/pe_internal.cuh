@@ -62,7 +62,12 @@ struct LaunchCtl {
     int32_t ready;      // unused (kept for layout)
     int32_t pad_;
     unsigned long long top_word;  // append look-back: epoch << 32 | stack top before the launch's pops
-    unsigned int pop_flag;        // = epoch E: some table pops (or may pop) at append launch E
+    // pop_flag[E & 1] = E: some table pops (or may pop) at append launch E.
+    // Written by launch E-1 into the slot launch E reads and never into the
+    // slot it reads itself (epochs alternate parity: period 0x3FFFFFFE), so a
+    // CTA that starts after another CTA of its own launch has finished still
+    // sees the previous launch's verdict.
+    unsigned int pop_flag[2];
 };
 
 // Launch table set: decode launches cover every sequence for layers

@@ -7,6 +7,7 @@
 namespace pe {
 
 constexpr int kAppendThreads = 128;      // 4 warps x 16 tables
+constexpr int kAppendEpochPeriod = 0x3FFFFFFE;  // K0 epochs 1..period: even, so consecutive epochs alternate parity
 constexpr int kEvictThreads = 128;       // 4 warps per CTA
 constexpr int kMaxPagesPerCta = 288;
 constexpr int kPrefillThreads = 128;     // score kernel: 4 warps per CTA
@@ -71,6 +72,17 @@ struct AttnArgs {
     int32_t* tickets;        // [n_tab] split completion tickets (zero between launches)
     int32_t layer, G, n_q_heads, splits, pages_per_split;
     float scale_log2;        // log2(e)/sqrt(d)
+    // Attention heads vs tables: launch item i = seq * kv_heads + h. A
+    // PER_KV_HEAD table holds one KV head (heads_per_table = 1); a PER_LAYER
+    // table holds every KV head of the layer, head h in columns
+    // [h*d, (h+1)*d) of each row (kv_vector.hpp:23-27; attention.cpp:23-35
+    // slices the concatenated row the same way).
+    int32_t kv_heads, heads_per_table, d;
+    __device__ __forceinline__ int table(const DevState& s, int i) const {
+        const int seq = i / kv_heads, h = i - seq * kv_heads;
+        return (seq * s.n_layers + layer) * s.tab_heads + h / heads_per_table;
+    }
+    __device__ __forceinline__ int col_elems(int i) const { return (i % kv_heads) % heads_per_table * d; }
 };
 __global__ void attention_split_kernel(DevState s, AttnArgs a);
 // tensor-core variant (bf16, B = 16, d in {64, 128}, G <= 8)

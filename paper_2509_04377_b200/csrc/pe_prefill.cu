@@ -896,7 +896,7 @@ __device__ __forceinline__ void copy_page_warp(const DevState& s, const PrefillA
 
 __global__ void __launch_bounds__(128) prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
     if (ctl->abort) return;
-    copy_page_warp(s, a, ctl, blockIdx.y, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+    copy_page_warp(s, a, ctl, blockIdx.x, blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5));
 }
 
 // ---------------------------------------------------------------------------

@@ -29,8 +29,9 @@ __device__ __forceinline__ void mbar_init_fence() {
 
 // One lane: order this thread's earlier generic-proxy reads of the stage
 // before the async-proxy writes, arm the barrier for `bytes`, and load the
-// `halves` 64-column boxes of box row `y` (page id * 32) into dst.
-__device__ __forceinline__ void tma_load_page(uint32_t dst, uint64_t* bar, const CUtensorMap* tmap, int y,
+// `halves` 64-column boxes of box row `y` (page id * 32), starting at column
+// `x0` (a PER_LAYER head's slice), into dst.
+__device__ __forceinline__ void tma_load_page(uint32_t dst, uint64_t* bar, const CUtensorMap* tmap, int y, int x0,
                                               int halves, uint32_t bytes) {
     const uint32_t b = smem_u32(bar);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -39,7 +40,7 @@ __device__ __forceinline__ void tma_load_page(uint32_t dst, uint64_t* bar, const
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
                 dst + hf * 4096),
-            "l"(tmap), "r"(hf * 64), "r"(y), "r"(b)
+            "l"(tmap), "r"(x0 + hf * 64), "r"(y), "r"(b)
             : "memory");
 }
 

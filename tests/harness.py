@@ -173,3 +173,27 @@ def compare_states(a: dict, b: dict, n_tables: int, B: int, check_pages=True, wh
             if check_pages:
                 np.testing.assert_array_equal(a["pages"][pid, :, :fill], b["pages"][pid, :, :fill],
                                               err_msg=f"{what}page bytes {pid}")
+
+
+def compare_states_vectorized(a: dict, b: dict, B: int, check_pages=True, what=""):
+    """compare_states for large engines (10^5+ tables): the same bit-exact
+    checks, vectorised over every mapped (table, logical page) slot."""
+    for key in ("num_pages", "newest_fill", "retained"):
+        np.testing.assert_array_equal(a[key], b[key], err_msg=f"{what}{key}")
+    np.testing.assert_array_equal(a["free_stack"], b["free_stack"], err_msg=f"{what}free list")
+    npg = a["num_pages"].astype(np.int64)
+    cols = np.arange(a["block_table"].shape[1])[None, :]
+    mapped = cols < npg[:, None]
+    np.testing.assert_array_equal(a["block_table"][mapped], b["block_table"][mapped],
+                                  err_msg=f"{what}block tables")
+    pids = a["block_table"][mapped].astype(np.int64)
+    # fill of each mapped page: B except the newest
+    is_newest = (cols == (npg[:, None] - 1))[mapped]
+    fill = np.where(is_newest, np.repeat(a["newest_fill"], npg), B)
+    slot_ok = np.arange(B)[None, :] < fill[:, None]
+    np.testing.assert_array_equal(np.where(slot_ok, a["positions"][pids], 0),
+                                  np.where(slot_ok, b["positions"][pids], 0), err_msg=f"{what}positions")
+    if check_pages:
+        m = slot_ok[:, None, :, None]
+        np.testing.assert_array_equal(np.where(m, a["pages"][pids], 0), np.where(m, b["pages"][pids], 0),
+                                      err_msg=f"{what}page bytes")
