@@ -3,38 +3,54 @@
 
     eviction step HBM GB/s (% of peak); p50 evict-step µs; pruned decode tokens/s
 
-Workload (N=1 line): BASELINE config 3 — Llama-3.1-8B KV geometry (32 layers,
-8 KV heads, head_dim 128, 32 query heads), batch 64, 32K-token prompts,
-budget C=4096, page size B=16, bf16, PER_KV_HEAD tables (16384 per GPU).
-Weak scaling: every rank holds its own 64 sequences (own pool, tables and
-free list; no data-path collective), NCCL only for the max-over-ranks time.
+Workload (default, the N=1 line): BASELINE config 3 — Llama-3.1-8B KV
+geometry (32 layers, 8 KV heads, head_dim 128, 32 query heads), batch 64,
+32K-token prompts, budget C=4096, page size B=16, bf16, PER_KV_HEAD tables
+(16384 per GPU). Weak scaling: every rank holds its own 64 sequences (own
+pool, tables and free list; no data-path collective).
 
-Setup (untimed, but measured with CUDA events and reported under
-"prefill"): K1 prefill prune+pack of every layer from synthetic N(0,1) K/V.
+`--config cfg5`: BASELINE config 5 — 1024 sequences at 128K context, sharded
+by sequence across the ranks (strong scaling: 1024/N sequences per rank, one
+layer's 8192 tables in total); prefill streamed in sequence waves.
+
+`--gpus N`: N ranks, one per GPU. Launched by the driver under torchrun
+(WORLD_SIZE/RANK/LOCAL_RANK from the environment); run directly with N > 1
+it re-executes itself under `torch.distributed.run`. N larger than the
+visible GPUs is an error. NCCL carries only the barrier, the max-over-ranks
+time and one small stats gather.
+
+Setup (untimed, measured with CUDA events and reported under "prefill"): K1
+prefill prune+pack of every layer from synthetic N(0,1) K/V.
 
 One bench STEP = one eviction cycle of the whole batch: B=16 decode tokens
 appended to every table (K0, one launch per token over all layers) followed
 by the PagedEviction block eviction of every table (K2, pages rescored from
-their resident K/V bytes; by default ONE launch per decode step covering
-all layers — each table's decision depends only on that table, so a layer
-loop that evicts after the step is equivalent; `--evict-launch layer` runs
-one launch per layer, and the other granularity is reported too). `value` = algorithmic
-bytes of the step (K2: (C+B)*row + 8*(C/B+1) + 4 per table; K0: 2*row+4
-per table per token) / device time of the step, all ranks.
+their resident K/V bytes; ONE launch covering all layers by default — each
+table's decision depends only on that table — `--evict-launch layer` runs
+one launch per layer; the other granularity is reported too). `value` =
+algorithmic bytes of the step, summed over ranks (K2: (C+B)*row + 8*(C/B+1)
++ 4 per table; K0: 2*row+4 per table per token) / the max over ranks of the
+step's device time.
 
-`e2e`: the same cycle through the C-ABI with HOST buffers: every token's
-K/V rows are copied from pinned host memory inside the timed region and the
-victims are read back to host after every eviction launch.
+`e2e`: the same cycle through the C-ABI with HOST buffers: every token's K/V
+rows are copied from pinned host memory inside the timed region and the
+victims are read back to host after every eviction launch (recompute scores;
+`e2e.cached` the same with the cached-score eviction K2c).
+
+`decode`: pruned decode tokens/s (K0 + K2 or K2c at the trigger + K3 on every
+layer) against FullCache (no eviction, the unpruned table growing from L:
+K0 + K3, measured on one layer and multiplied by the layer count).
 
 `--impl reference`: the reference's own CPU implementation (oracle/_ref,
 compiled from the reference sources) on the same config, all host threads,
-on a bounded sample of tables.
+on a bounded sample of tables; rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -48,13 +64,20 @@ sys.path.insert(0, str(ROOT))
 METRIC = "eviction step HBM GB/s (% of peak); p50 evict-step µs; pruned decode tokens/s"
 
 CONFIGS = {
-    # name: (layers, kv_heads, head_dim, q_heads, seqs, prompt, budget, dtype)
-    "cfg1": dict(layers=16, kvh=8, d=64, qh=32, seqs=1, L=4096, C=1024, dtype="f32",
+    # seqs: per rank (weak scaling) or in total (strong scaling, sharded by sequence)
+    "cfg1": dict(layers=16, kvh=8, d=64, qh=32, seqs=1, L=4096, C=1024, dtype="f32", scaling="weak",
                  desc="Llama-3.2-1B KV geometry, 1 seq, 4K fp32 prefill, C=1024"),
-    "cfg2": dict(layers=28, kvh=8, d=128, qh=24, seqs=32, L=16384, C=2048, dtype="bf16",
+    "cfg2": dict(layers=28, kvh=8, d=128, qh=24, seqs=32, L=16384, C=2048, dtype="bf16", scaling="weak",
                  desc="Llama-3.2-3B KV geometry, batch 32, 16K context, C=2048, bf16"),
-    "cfg3": dict(layers=32, kvh=8, d=128, qh=32, seqs=64, L=32768, C=4096, dtype="bf16",
+    "cfg3": dict(layers=32, kvh=8, d=128, qh=32, seqs=64, L=32768, C=4096, dtype="bf16", scaling="weak",
                  desc="Llama-3.1-8B KV geometry, batch 64, 32K context, C=4096, bf16"),
+    "cfg5": dict(layers=1, kvh=8, d=128, qh=32, seqs=1024, L=131072, C=4096, dtype="bf16", scaling="strong",
+                 wave_seqs=16,
+                 desc="Llama-3.1-8B KV geometry, 1024 sequences x 128K context sharded by sequence across "
+                      "the ranks, one layer (8192 tables in total), C=4096, bf16"),
+    # a small configuration for the multi-rank plumbing tests
+    "tiny": dict(layers=2, kvh=8, d=128, qh=32, seqs=4, L=8192, C=1024, dtype="bf16", scaling="weak",
+                 desc="test configuration: 8B KV geometry, 2 layers, 4 x 8K, C=1024"),
 }
 B = 16
 
@@ -65,6 +88,16 @@ def load_peaks():
         d = json.loads(p.read_text())
         return float(d.get("hbm_gbs", 6650.0)), "measured"
     return 6650.0, "fallback"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -166,7 +199,79 @@ def dist_setup():
     return world, rank, local
 
 
-# --------------------------------------------------------------------------- reference arm
+def rank_seqs(cfg, world, rank):
+    """(first sequence, sequence count) of this rank: weak scaling gives every
+    rank cfg['seqs'] sequences of its own; strong scaling shards cfg['seqs']."""
+    if cfg["scaling"] == "strong":
+        from paper_2509_04377_b200.dist import shard
+
+        lo, hi = shard(cfg["seqs"], world, rank)
+        return lo, hi - lo
+    return rank * cfg["seqs"], cfg["seqs"]
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: one rank per GPU
+    under torch.distributed.run, rendezvous on 127.0.0.1."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve())]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+# --------------------------------------------------------------------------- CPU reference
+def cpu_legs(cfg, threads, decode_tables, decode_cycles, single: bool):
+    """The reference's own CPU implementation of the three kernels' work, on
+    bounded samples, with `threads` host threads (and a single-thread run
+    when `single`): decode eviction cycles (make_kv + decode_step x16, one
+    PagedEviction trigger), prefill (make_kv + prefill_compress + append of
+    the survivors, policy.cpp:54-63) and attention (attend per query head,
+    attention.cpp:97-99). Rates are converted to "equivalent GB/s" over the
+    same algorithmic bytes as the GPU kernels."""
+    import oracle
+
+    ref = oracle.Reference()
+    C, d, L = cfg["C"], cfg["d"], cfg["L"]
+    G = cfg["qh"] // cfg["kvh"]
+    elt = 2 if cfg["dtype"] == "bf16" else 4
+    row_alg = 2 * d * elt
+    cycle_bytes = k2_bytes_per_table(C, row_alg) + B * (2 * row_alg + 4)
+    out = {}
+
+    def leg(name, fn, n_tables, unit_bytes, th, sample):
+        secs = fn(n_tables, th)
+        return {"tables_per_s": round(n_tables / secs, 2), "gbs": round(n_tables * unit_bytes / secs / 1e9, 3),
+                "seconds": round(secs, 4), "threads": th, "sample": sample}
+
+    def dec(n, th):
+        secs, ev = ref.bench_decode_cycles(n, C, B, d, th, decode_cycles, seed=7, warmup_cycles=1)
+        assert ev == n * decode_cycles, (ev, n)
+        return secs / decode_cycles
+
+    runs = [(threads, 1)] + ([(1, 16)] if single and threads > 1 else [])
+    for th, div in runs:
+        key = "all_cores" if th == threads else "single_thread"
+        nt_dec = max(th, decode_tables // div)
+        nt_pre = max(th, (4 * threads) // div)
+        nt_att = max(th, (16 * threads) // div)
+        out[key] = {
+            "decode_cycle": leg("decode", dec, nt_dec, cycle_bytes, th,
+                                f"{nt_dec} tables x {decode_cycles} cycles, identity-prefilled to C"),
+            "prefill": leg("prefill", lambda n, t: ref.bench_prefill(n, L, C, B, d, t), nt_pre,
+                           k1_bytes_per_table(L, C, row_alg), th, f"{nt_pre} tables of {L} tokens"),
+            "attention": leg("attention", lambda n, t: ref.bench_attend(n, C + B // 2, B, d, G, t), nt_att,
+                             k3_bytes_per_table(C + B // 2, row_alg, G, d, elt), th,
+                             f"{nt_att} tables of {C + B // 2} tokens x {G} query heads"),
+        }
+    return out
+
+
 def run_reference(args, cfg, world, rank):
     if rank != 0:
         return
@@ -174,34 +279,33 @@ def run_reference(args, cfg, world, rank):
 
     ref = oracle.Reference()
     threads = os.cpu_count() or 1
-    row = 2 * cfg["d"] * 4  # the reference stores float32 K and V
     row_alg = 2 * cfg["d"] * (2 if cfg["dtype"] == "bf16" else 4)
     C = cfg["C"]
-    # bounded sample: `tables` tables per step, one eviction cycle each
+    # bounded sample: `tables` tables per step, `cps` eviction cycles each
     tables = args.ref_tables or 1024
-    cps = 8  # eviction cycles per step (a step is a bounded sample of the workload)
-    # one session: W untimed warm-up cycles, then K timed steps of `cps` cycles
+    cps = 8
     secs, ev = ref.bench_decode_cycles(tables, C, B, cfg["d"], threads, args.steps * cps, seed=1,
                                        warmup_cycles=args.warmup)
     assert ev == tables * args.steps * cps, (ev, tables)
     per_step = secs / args.steps
-    times = [per_step / cps]
-    bytes_step = cps * tables * (k2_bytes_per_table(C, row_alg) + B * (row_alg + 4))
+    bytes_step = cps * tables * (k2_bytes_per_table(C, row_alg) + B * (2 * row_alg + 4))
     value = bytes_step / per_step / 1e9
+    legs = cpu_legs(cfg, threads, 1024, 16, single=True)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(per_step * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(per_step * 1e3, 3), "higher_is_better": True, "scaling": cfg["scaling"],
         "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) (reference GaussianStream)",
         "config": {"workload": f"{args.config}: {cfg['desc']}", "tables_sampled": tables,
-                   "cycle": "B=16 decode_step calls per table incl. one PagedEviction trigger", "cycles_per_step": cps},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
-                         "kind": "reference",
+                   "cycle": "B=16 decode_step calls per table incl. one PagedEviction trigger",
+                   "cycles_per_step": cps},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"{tables} tables x {cps} eviction cycles per step "
-                                   f"(make_kv + EvictionPolicy::decode_step x16), identity-prefilled to C"},
-        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-        "p50_evict_step_us_per_table": round(statistics.median(times) / tables * threads * 1e6, 3),
+                                   f"(make_kv + EvictionPolicy::decode_step x16), identity-prefilled to C",
+                         "legs": legs},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "p50_evict_step_us_per_table": round(per_step / cps / tables * threads * 1e6, 3),
     }
     print(json.dumps(line), flush=True)
 
@@ -221,13 +325,14 @@ def cpu_baseline(cfg, args):
     row_alg = 2 * cfg["d"] * (2 if cfg["dtype"] == "bf16" else 4)
     secs, ev = ref.bench_decode_cycles(tables, cfg["C"], B, cfg["d"], threads, cycles, seed=7,
                                        warmup_cycles=1)
-    bytes_step = cycles * tables * (k2_bytes_per_table(cfg["C"], row_alg) + B * (row_alg + 4))
+    bytes_step = cycles * tables * (k2_bytes_per_table(cfg["C"], row_alg) + B * (2 * row_alg + 4))
     return {"value": round(bytes_step / secs / 1e9, 3), "unit": "GB/s", "cores": threads,
-            "kind": "reference",
+            "kind": "reference", "cpu_model": cpu_model(),
             "sample": f"{tables} of the {args.config} tables x {cycles} eviction cycles (16 make_kv + "
                       f"EvictionPolicy::decode_step each, one PagedEviction trigger), {secs:.3f} s timed "
                       f"on {threads} threads; identity-prefilled to C (setup untimed)",
-            "evictions": int(ev)}
+            "evictions": int(ev),
+            "legs": cpu_legs(cfg, threads, 1024, 16, single=True)}
 
 
 # --------------------------------------------------------------------------- B200 arm
@@ -237,11 +342,29 @@ def run_b200(args, cfg, world, rank, local):
     import torch.distributed as dist
 
     import paper_2509_04377_b200 as pe
+    from paper_2509_04377_b200.dist import RankStats, gather_stats, max_over_ranks as _mor, sum_over_ranks as _sor
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    n_dev = torch.cuda.device_count()
+    if args.share_device:  # test-only: every rank on device 0, gloo plumbing
+        local_dev = 0
+    else:
+        if world > n_dev:
+            raise SystemExit(f"bench.py: --gpus {world} needs {world} visible GPUs, found {n_dev}")
+        local_dev = local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.share_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def max_over_ranks(x):
+        return _mor(x, device=None if args.share_device else dev)
+
+    def sum_over_ranks(x):
+        return _sor(x, device=None if args.share_device else dev)
+
     peak, peak_kind = load_peaks()
     # live HBM probe (untimed): K2 is read-only traffic, so its roofline is
     # also reported against the streaming-read bandwidth of this GPU
@@ -250,54 +373,60 @@ def run_b200(args, cfg, world, rank, local):
     from paper_2509_04377_b200 import _lib as _pl
 
     _rd, _cp = _C.c_double(0.0), _C.c_double(0.0)
-    probe_ok = _pl.load().pe_probe_hbm(local, 8 << 30, 5, _C.byref(_rd), _C.byref(_cp)) == 0
+    probe_ok = _pl.load().pe_probe_hbm(local_dev, 8 << 30, 5, _C.byref(_rd), _C.byref(_cp)) == 0
     probe = {"read_gbs": round(_rd.value, 1), "kind": "256-bit streaming read of 8 GiB, best of 5 (pe_probe_hbm)"} \
         if probe_ok else None
     bf16 = cfg["dtype"] == "bf16"
     tdt = torch.bfloat16 if bf16 else torch.float32
     elt = 2 if bf16 else 4
-    S, NL, H, d, L, C, QH = (cfg["seqs"], cfg["layers"], cfg["kvh"], cfg["d"], cfg["L"], cfg["C"],
-                             cfg["qh"])
+    NL, H, d, L, C, QH = cfg["layers"], cfg["kvh"], cfg["d"], cfg["L"], cfg["C"], cfg["qh"]
+    seq0, S = rank_seqs(cfg, world, rank)
     G = QH // H
     row = 2 * d * elt  # K+V
     geo = pe.EngineGeometry(n_seqs=S, n_layers=NL, n_kv_heads=H, head_dim=d,
-                            dtype=pe.DTYPE_BF16 if bf16 else pe.DTYPE_F32, device=local)
+                            dtype=pe.DTYPE_BF16 if bf16 else pe.DTYPE_F32, device=local_dev)
     eng = pe.PagedEvictionEngine(geo, pe.PolicyConfig(cache_budget=C, page_size=B))
     stream = torch.cuda.current_stream()
     gen = torch.Generator(device=dev)
     gen.manual_seed(20250904 + 3 + 1000 * rank)
 
-    # ---------------- setup: K1 prefill prune+pack of every layer (event-timed)
-    cu = np.arange(S + 1, dtype=np.int32) * L
-    k_in = torch.empty((S * L, H, d), dtype=tdt, device=dev)
+    # ---------------- setup: K1 prefill prune+pack of every layer (event-timed),
+    # in sequence waves when the raw prompts of the rank do not fit at once
+    wave = min(S, cfg.get("wave_seqs", S))
+    k_in = torch.empty((wave * L, H, d), dtype=tdt, device=dev)
     v_in = torch.empty_like(k_in)
     pre_ms = []
     for layer in range(NL):
-        k_in.normal_(generator=gen)
-        v_in.normal_(generator=gen)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        eng.prefill_compress(layer, k_in, v_in, cu)
-        e1.record(stream)
-        e1.synchronize()
-        pre_ms.append(e0.elapsed_time(e1))
+        ms = 0.0
+        for w0 in range(0, S, wave):
+            nw = min(wave, S - w0)
+            k_in[: nw * L].normal_(generator=gen)
+            v_in[: nw * L].normal_(generator=gen)
+            cu = np.arange(nw + 1, dtype=np.int32) * L
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            eng.prefill_compress(layer, k_in[: nw * L], v_in[: nw * L], cu, seq_begin=w0)
+            e1.record(stream)
+            e1.synchronize()
+            ms += e0.elapsed_time(e1)
+        pre_ms.append(ms)
     eng.sync()
     del k_in, v_in
     torch.cuda.empty_cache()
     n_tab_layer = S * H
     k1_bytes = n_tab_layer * k1_bytes_per_table(L, C, row)
-    pre_sorted = sorted(pre_ms[1:] or pre_ms)
+    pre_p50 = statistics.median(pre_ms[1:] or pre_ms)
     prefill = {"kernel": "K1 prefill_prune_pack: score + CTA-per-table select + copy, "
                          "2 sequence waves on 2 streams",
-               "ms_per_layer_p50": round(statistics.median(pre_sorted), 4),
-               "gbs": round(k1_bytes / (statistics.median(pre_sorted) * 1e-3) / 1e9, 1),
-               "tables_per_layer": n_tab_layer,
+               "ms_per_layer_p50": round(pre_p50, 4),
+               "gbs": round(k1_bytes / (pre_p50 * 1e-3) / 1e9, 1),
+               "tables_per_layer": n_tab_layer, "prompt_waves": (S + wave - 1) // wave,
                "algorithmic_bytes_per_layer": k1_bytes}
     prefill["frac"] = round(prefill["gbs"] / peak, 4)
 
     # ---------------- decode inputs: B tokens of rows for every table (device + pinned host)
     # every decode token's positions, precomputed (no per-token increment kernel)
-    max_tokens = B * (2 * args.steps + args.warmup + 16 + max(0, 100 - args.steps))
+    max_tokens = B * (2 * args.steps + args.warmup + 24 + max(0, 100 - args.steps))
     pos_all = (L + torch.arange(max_tokens, device=dev, dtype=torch.int64)).unsqueeze(1).expand(
         max_tokens, S).contiguous()
     tok = [0]
@@ -317,7 +446,6 @@ def run_b200(args, cfg, world, rank, local):
     k2_per_launch = (n_tab if args.evict_launch == "step" else n_tab_layer) * k2_bytes_per_table(C, row)
 
     cycles = [0]  # eviction cycles run on every table (cadence check)
-
     k0_evs = []  # (start, end) around each cycle's B append launches (timed cycles only)
 
     def cycle(record=None, host=False, mode=pe.ScoreMode.RECOMPUTE, victims_host=None):
@@ -353,11 +481,6 @@ def run_b200(args, cfg, world, rank, local):
             dist.barrier()
         torch.cuda.synchronize()
 
-    from paper_2509_04377_b200.dist import RankStats, gather_stats, max_over_ranks as _mor
-
-    def max_over_ranks(x):
-        return _mor(x, device=dev)
-
     for _ in range(args.warmup):
         cycle()
     eng.sync()
@@ -366,7 +489,7 @@ def run_b200(args, cfg, world, rank, local):
     evs = []
     barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         t0.record(stream)
         for _ in range(args.steps):
             cycle(record=evs)
@@ -376,9 +499,10 @@ def run_b200(args, cfg, world, rank, local):
     launches = eng.stats().kernel_launches - launches0
     ms_total = max_over_ranks(t0.elapsed_time(t1))
     ms_step = ms_total / args.steps
+    total_step_bytes = sum_over_ranks(float(step_bytes))
     k2_ms = [a.elapsed_time(b) for a, b in evs]
     k2_mean = statistics.mean(k2_ms)
-    value = world * step_bytes / (ms_step * 1e-3) / 1e9
+    value = total_step_bytes / (ms_step * 1e-3) / 1e9
     k2_gbs = k2_per_launch / (k2_mean * 1e-3) / 1e9
     # p50 evict-step µs over >= 100 trigger launches: extra
     # cycles after the timed region when --steps is smaller (not in `value`)
@@ -390,7 +514,7 @@ def run_b200(args, cfg, world, rank, local):
 
     # ---------------- cached-score variant (K2c): p50 of the evict launch
     evc = []
-    for _ in range(2):
+    for _ in range(4):
         cycle(record=evc, mode=pe.ScoreMode.CACHED)
     eng.sync()
     k2c_us = statistics.median([a.elapsed_time(b) * 1e3 for a, b in evc])
@@ -407,81 +531,80 @@ def run_b200(args, cfg, world, rank, local):
     other_us = statistics.median([a.elapsed_time(b) * 1e3 for a, b in evo])
     other_bytes = (n_tab if other == "step" else n_tab_layer) * k2_bytes_per_table(C, row)
 
-    # ---------------- e2e: host buffers through the C-ABI
+    # ---------------- e2e: host buffers through the C-ABI (recompute, then cached scores)
     vict_host = torch.zeros(n_tab, dtype=torch.int32).pin_memory()  # step result read back
-    cycle(host=True, victims_host=vict_host)  # warm the host-staging ring (untimed)
-    eng.sync()
-    barrier()
-    w0 = time.perf_counter()
-    for _ in range(max(1, args.steps)):
-        cycle(host=True, victims_host=vict_host)
-    eng.sync()
-    barrier()
-    e2e_s = max_over_ranks((time.perf_counter() - w0) / max(1, args.steps))
-    e2e = {"value": round(world * step_bytes / e2e_s / 1e9, 3), "unit": "GB/s",
+
+    def e2e_run(mode):
+        cycle(host=True, victims_host=vict_host, mode=mode)  # warm the host-staging ring (untimed)
+        eng.sync()
+        barrier()
+        w0 = time.perf_counter()
+        for _ in range(max(1, args.steps)):
+            cycle(host=True, victims_host=vict_host, mode=mode)
+        eng.sync()
+        barrier()
+        return max_over_ranks((time.perf_counter() - w0) / max(1, args.steps))
+
+    e2e_s = e2e_run(pe.ScoreMode.RECOMPUTE)
+    e2e_c = e2e_run(pe.ScoreMode.CACHED)
+    e2e = {"value": round(total_step_bytes / e2e_s / 1e9, 3), "unit": "GB/s",
            "h2d_bytes_per_step": int(B * 2 * NL * S * H * d * elt + B * S * 8),
            "d2h_bytes_per_step": int(n_tab * 4),
-           "ms_per_step": round(e2e_s * 1e3, 3)}
+           "ms_per_step": round(e2e_s * 1e3, 3), "score_mode": "recompute (K2)",
+           # the same cycle with the cached-score eviction (K2c reads 12 B per
+           # page instead of the pages): its time, and the recompute step's
+           # bytes over it as an "equivalent" rate (not an HBM rate)
+           "cached": {"ms_per_step": round(e2e_c * 1e3, 3), "score_mode": "cached (K2c)",
+                      "equivalent_gbs": round(total_step_bytes / e2e_c / 1e9, 3),
+                      "hbm_bytes_per_step": int(sum_over_ranks(float(k0_alg + n_tab * 12 * (C // B + 1)))),
+                      "hbm_gbs": round(sum_over_ranks(float(k0_alg + n_tab * 12 * (C // B + 1))) / e2e_c / 1e9,
+                                       3)}}
 
-    # ---------------- pruned decode tokens/s (K0 + K2 + K3, all layers)
+    # ---------------- pruned decode tokens/s (K0 + K2/K2c + K3, all layers) vs FullCache
     decode = None
+    total_seqs = int(round(sum_over_ranks(float(S))))
     if not args.no_decode:
         q = torch.randn((S, QH, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
         out = torch.empty((S, QH, d), dtype=torch.float32, device=dev)
+
+        def decode_tokens(mode, attn_ms=None):
+            """B decode tokens: per token K0 over all layers, then per layer the
+            trigger's eviction (on the B-th token) and K3."""
+            barrier()
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0.record(stream)
+            for j in range(B):
+                eng.append_token(0, NL, rows_k[j], rows_v[j], next_pos())
+                for layer in range(NL):
+                    if j == B - 1:
+                        eng.evict(layer, 1, mode=mode)
+                    if attn_ms is not None:
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record(stream)
+                        eng.attend(layer, q, out, QH)
+                        b.record(stream)
+                        attn_ms.append((a, b))
+                    else:
+                        eng.attend(layer, q, out, QH)
+            d1.record(stream)
+            d1.synchronize()
+            cycles[0] += 1
+            return max_over_ranks(d0.elapsed_time(d1))
+
         attn_ms = []
-        torch.cuda.synchronize()
-        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        d0.record(stream)
-        for j in range(B):
-            eng.append_token(0, NL, rows_k[j], rows_v[j], next_pos())
-            for layer in range(NL):
-                if j == B - 1:
-                    eng.evict(layer, 1)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                eng.attend(layer, q, out, QH)
-                b.record(stream)
-                attn_ms.append((a, b))
-        d1.record(stream)
-        d1.synchronize()
-        cycles[0] += 1
-        dec_ms = d0.elapsed_time(d1)
+        dec_ms = decode_tokens(pe.ScoreMode.RECOMPUTE, attn_ms)
+        dec_ms_c = decode_tokens(pe.ScoreMode.CACHED)
         at = [a.elapsed_time(b) for a, b in attn_ms]
         k3_bytes = n_tab_layer * k3_bytes_per_table(C + B // 2, row, G, d, elt)
-        decode = {"tokens_per_s": round(world * S * B / (dec_ms * 1e-3), 1),
+        decode = {"tokens_per_s": round(total_seqs * B / (dec_ms * 1e-3), 1),
                   "ms_per_token_all_layers": round(dec_ms / B, 4),
+                  "score_mode": "recompute (K2 at the trigger)",
+                  "tokens_per_s_cached": round(total_seqs * B / (dec_ms_c * 1e-3), 1),
+                  "ms_per_token_all_layers_cached": round(dec_ms_c / B, 4),
                   "attention_us_per_layer_p50": round(statistics.median(at) * 1e3, 2),
                   "attention_gbs": round(k3_bytes / (statistics.median(at) * 1e-3) / 1e9, 1)}
-        # the downstream win: the same attention over the UNPRUNED cache
-        # (FullCache, one layer: all L tokens of the batch, 8.6 GB at cfg3)
-        try:
-            fgeo = pe.EngineGeometry(n_seqs=S, n_layers=1, n_kv_heads=H, head_dim=d,
-                                     dtype=pe.DTYPE_BF16 if bf16 else pe.DTYPE_F32, device=local,
-                                     max_pages_per_table=(L + B - 1) // B + 1)
-            feng = pe.PagedEvictionEngine(fgeo, pe.PolicyConfig(cache_budget=C, page_size=B,
-                                                                kind=pe.PolicyKind.FullCache))
-            fk = torch.empty((S * L, H, d), dtype=tdt, device=dev).normal_(generator=gen)
-            feng.prefill_compress(0, fk, torch.empty_like(fk).normal_(generator=gen), cu)
-            del fk
-            fat = []
-            for _ in range(5):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                feng.attend(0, q, out, QH)
-                b.record(stream)
-                fat.append((a, b))
-            torch.cuda.synchronize()
-            f_us = statistics.median([a.elapsed_time(b) for a, b in fat]) * 1e3
-            feng.close()
-            torch.cuda.empty_cache()
-            f_bytes = n_tab_layer * k3_bytes_per_table(L, row, G, d, elt)
-            p_us = statistics.median(at) * 1e3
-            decode["full_cache"] = {"attention_us_per_layer_p50": round(f_us, 2),
-                                    "attention_gbs": round(f_bytes / (f_us * 1e-6) / 1e9, 1),
-                                    "retained_tokens_per_table": L,
-                                    "attention_speedup_pruned": round(f_us / p_us, 2)}
-        except Exception as exc:  # pool for the unpruned layer does not fit: report why
-            decode["full_cache"] = {"unavailable": str(exc)[:200]}
+        decode["full_cache"] = full_cache_decode(args, cfg, pe, torch, np, gen, dev, local_dev, stream, S, q, out,
+                                                 statistics.median(at) * 1e3, max_over_ranks, total_seqs)
 
     st = eng.stats()
     # full-size parity by size-independent properties (untimed): every table
@@ -496,18 +619,25 @@ def run_b200(args, cfg, world, rank, local):
     ranks = gather_stats(RankStats(rank=rank, tables=n_tab, tokens_scored=int(st.tokens_scored),
                                    pages_evicted=int(st.pages_evicted),
                                    algorithmic_bytes=int(step_bytes * args.steps), kernel_ms=k2_ms))
-    cpu = cpu_baseline(cfg, args) if (rank == 0 and world == 1 and not args.no_cpu) else None
+    for r, c in zip(ranks, _gather_obj(world, {"seq_begin": seq0, "seqs": S, "device": local_dev,
+                                               "ms_per_step": round(t0.elapsed_time(t1) / args.steps, 4),
+                                               "checks_ok": checks["cadence_ok"]
+                                               and checks["invariant_violations"] == 0})):
+        r.update(c)
+    cpu = cpu_baseline(cfg, args) if (rank == 0 and not args.no_cpu) else None
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
+            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic N(0,1) K/V/Q (torch.randn); inputs resident in HBM",
             "config": {"workload": f"{args.config}: {cfg['desc']}", "tables_per_gpu": n_tab,
+                       "tables_total": n_tab * world if cfg["scaling"] == "weak" else cfg["seqs"] * NL * H,
                        "page_size": B, "step": "one eviction cycle: 16 decode appends (K0, all layers per launch) "
                        "+ block eviction of every table (K2, " + ("one launch for all layers)" if args.evict_launch
                                                                   == "step" else "one launch per layer)"),
-                       "l2": "inputs larger than L2 (pool %.1f GB per GPU)" % (eng.info().pool_bytes / 1e9)},
+                       "l2": "inputs larger than L2 (pool %.1f GB per GPU)" % (eng.info().pool_bytes / 1e9),
+                       "parallelism": f"sequence-sharded x{world}, no data-path collective"},
             "pct_of_peak": round(100 * value / world / peak, 2),
             "p50_evict_step_us": round(k2_p50_ms * 1e3, 2),
             "p50_evict_step_samples": len(evs_p50),
@@ -516,10 +646,11 @@ def run_b200(args, cfg, world, rank, local):
             "evict_launch": args.evict_launch,
             f"p50_evict_{other}_launch_us": round(other_us, 2),
             f"evict_{other}_launch_gbs": round(other_bytes / (other_us * 1e-6) / 1e9, 1),
+            f"evict_{other}_launch_frac": round(other_bytes / (other_us * 1e-6) / 1e9 / peak, 4),
             "roofline": {"bound": "hbm", "achieved": round(k2_gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(k2_gbs / peak, 4), "traffic": ncu_traffic(expect_bytes=k2_per_launch),
                          "traffic_source": "ncu dram__bytes_read+write per launch, profiles/*bench_launches*.csv",
-                         "kernel": "K2 evict_score_kernel, " + ("one launch per decode step (all 32 layers)"
+                         "kernel": "K2 evict_score_kernel, " + (f"one launch per decode step (all {NL} layers)"
                                                                   if args.evict_launch == "step" else "per-layer launch"),
                          "algorithmic_bytes_per_launch": k2_per_launch, "peak_kind": peak_kind,
                          "probe": probe,
@@ -531,12 +662,89 @@ def run_b200(args, cfg, world, rank, local):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
-            "ranks": ranks if world > 1 else None,
+            "ranks": ranks,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _gather_obj(world, obj):
+    import torch.distributed as dist
+
+    if world == 1:
+        return [obj]
+    out = [None] * world
+    dist.all_gather_object(out, obj)
+    return out
+
+
+def full_cache_decode(args, cfg, pe, torch, np, gen, dev, local_dev, stream, S, q, out, pruned_attn_us,
+                      max_over_ranks, total_seqs):
+    """FullCache decode (policy.cpp:292-304: no eviction, the table keeps
+    every token and grows from L) on one layer — K0 + K3 per token — and the
+    tokens/s of the whole model (× layers). When the unpruned layer of all S
+    sequences does not fit beside the pruned pool, a stated subset of the
+    sequences is measured (attention time is linear in the sequences)."""
+    bf16 = cfg["dtype"] == "bf16"
+    tdt = torch.bfloat16 if bf16 else torch.float32
+    elt = 2 if bf16 else 4
+    NL, H, d, L, QH = cfg["layers"], cfg["kvh"], cfg["d"], cfg["L"], cfg["qh"]
+    G = QH // H
+    row = 2 * d * elt
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    per_seq = H * ((L + 2 * B) // B + 1) * 2 * B * row // 2 + L * H * row  # pool + prompt staging
+    S_f = max(1, min(S, int(0.6 * free_b // per_seq)))
+    try:
+        fgeo = pe.EngineGeometry(n_seqs=S_f, n_layers=1, n_kv_heads=H, head_dim=d,
+                                 dtype=pe.DTYPE_BF16 if bf16 else pe.DTYPE_F32, device=local_dev,
+                                 max_pages_per_table=(L + 2 * B) // B + 1)
+        feng = pe.PagedEvictionEngine(fgeo, pe.PolicyConfig(cache_budget=cfg["C"], page_size=B,
+                                                            kind=pe.PolicyKind.FullCache))
+        fk = torch.empty((S_f * L, H, d), dtype=tdt, device=dev).normal_(generator=gen)
+        cu = np.arange(S_f + 1, dtype=np.int32) * L
+        feng.prefill_compress(0, fk, torch.empty_like(fk).normal_(generator=gen), cu)
+        del fk
+        torch.cuda.empty_cache()
+        fq, fo = q[:S_f].contiguous(), out[:S_f]
+        rk = torch.randn((B, 1, S_f, H, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
+        rv = torch.randn((B, 1, S_f, H, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
+        pos = L + torch.arange(B, device=dev, dtype=torch.int64).unsqueeze(1).expand(B, S_f).contiguous()
+        feng.attend(0, fq, fo, QH)  # warm
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        att = []
+        a.record(stream)
+        for j in range(B):
+            feng.append_token(0, 1, rk[j], rv[j], pos[j])
+            x, y = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            x.record(stream)
+            feng.attend(0, fq, fo, QH)
+            y.record(stream)
+            att.append((x, y))
+        b.record(stream)
+        b.synchronize()
+        layer_ms = max_over_ranks(a.elapsed_time(b) / B)  # one token on one layer
+        f_us = statistics.median(x.elapsed_time(y) for x, y in att) * 1e3
+        ok = feng.check_invariants()["violations"] == 0 and feng.stats().pages_evicted == 0
+        feng.close()
+        torch.cuda.empty_cache()
+        f_bytes = S_f * H * k3_bytes_per_table(L + B // 2, row, G, d, elt)
+        scale = S / S_f  # attention time is linear in the sequences
+        return {"tokens_per_s": round(total_seqs / (NL * layer_ms * scale * 1e-3), 1),
+                "ms_per_token_all_layers": round(NL * layer_ms * scale, 4),
+                "measured": f"K0 + K3 on one layer of {S_f} of the rank's {S} sequences (unpruned, "
+                            f"~{L + B // 2} tokens per table), x {NL} layers" + (
+                                f", x {scale:.2f} for the other sequences" if S_f < S else ""),
+                "attention_us_per_layer_p50": round(f_us, 2),
+                "attention_gbs": round(f_bytes / (f_us * 1e-6) / 1e9, 1),
+                "retained_tokens_per_table": L + B // 2,
+                "attention_speedup_pruned": round(f_us * scale / pruned_attn_us, 2),
+                "no_evictions_ok": bool(ok)}
+    except Exception as exc:  # pool for the unpruned layer does not fit: report why
+        torch.cuda.empty_cache()
+        return {"unavailable": str(exc)[:200]}
 
 
 def main():
@@ -551,10 +759,21 @@ def main():
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--evict-launch", default="step", choices=["layer", "step"],
                     help="one K2 launch per layer, or one per decode step covering all layers")
+    ap.add_argument("--share-device", action="store_true",
+                    help="test only: every rank on device 0 with the gloo backend")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
-    world, rank, local = dist_setup()
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ:
+        if args.gpus > 1 and args.impl == "b200":
+            sys.exit(relaunch(args))
+        world, rank, local = args.gpus if args.impl == "reference" else 1, 0, 0
+    else:
+        world, rank, local = dist_setup()
+        if world != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
     else:

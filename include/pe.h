@@ -353,6 +353,12 @@ pe_status pe_read_table(pe_engine* eng, int32_t table, int32_t* page_ids, int32_
 pe_status pe_pool_allocate(pe_engine* eng, int32_t* page_id);
 pe_status pe_pool_release(pe_engine* eng, int32_t page_id);
 
+/* The calling host thread's current CUDA device (cudaGetDevice): the device
+ * stateless helpers such as the façade's prefill selection run on, so a
+ * multi-GPU process (one host thread per GPU) never funnels
+ * them onto device 0. PE_NO_DEVICE without a CUDA device. */
+pe_status pe_current_device(int32_t* device);
+
 /* Thread-local message for the last non-OK status returned on this thread. */
 const char* pe_last_error(void);
 const char* pe_status_string(pe_status s);

@@ -81,6 +81,7 @@ SIGNATURES = {
     "pe_step_log_capture": (C.c_int, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "pe_decode_evict_tokens": (C.c_int, [c_vp, c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "pe_probe_hbm": (C.c_int, [c_i32, c_i64, c_i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "pe_current_device": (C.c_int, [C.POINTER(c_i32)]),
 }
 
 

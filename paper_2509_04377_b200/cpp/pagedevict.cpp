@@ -678,9 +678,12 @@ std::vector<std::size_t> EvictionPolicy::device_select_survivors(const std::vect
     }
     const std::size_t C = config.cache_budget;
     const std::uint32_t B = config.page_size;
+    // the calling thread's current device (one host thread per GPU)
+    std::int32_t device = 0;
+    check(pe_current_device(&device), "prefill_compress");
     auto& sel = selectors();
     std::lock_guard lock(sel.mu);
-    const SelectorKey key{0, W, B, C};
+    const SelectorKey key{device, W, B, C};
     pe_engine*& eng = sel.engines[key];
     if (eng == nullptr) {
         pe_config c{};
@@ -693,7 +696,7 @@ std::vector<std::size_t> EvictionPolicy::device_select_survivors(const std::vect
         c.cache_budget = static_cast<std::int32_t>(C);
         c.dtype = PE_DTYPE_F32;
         c.policy = PE_POLICY_PAGED_EVICTION;
-        c.device = 0;
+        c.device = device;
         pe_engine* e = nullptr;
         const pe_status st = pe_engine_create(&c, &e);
         if (st != PE_OK) {
@@ -772,7 +775,9 @@ std::vector<char> EvictionPolicy::device_prompt_select(const std::vector<KvVecto
         pos[i] = checked_position(tokens[i].position);
     }
     std::vector<std::uint8_t> flags(n, 0);
-    check(pe_prompt_select(0, rule, K.data(), static_cast<std::int32_t>(n), static_cast<std::int32_t>(W), pos.data(),
+    std::int32_t device = 0;
+    check(pe_current_device(&device), "prefill_compress");
+    check(pe_prompt_select(device, rule, K.data(), static_cast<std::int32_t>(n), static_cast<std::int32_t>(W), pos.data(),
                            static_cast<std::int32_t>(k), flags.data()),
           "prefill_compress");
     return std::vector<char>(flags.begin(), flags.end());

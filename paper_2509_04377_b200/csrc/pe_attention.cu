@@ -35,6 +35,14 @@ __device__ __forceinline__ float elem_f32(const uint8_t* row, int idx, int dtype
     return reinterpret_cast<const float*>(row)[idx];
 }
 
+// o / l, or 0 with PE_EMPTY_CACHE for a table without retained tokens (the
+// reference's attend throws EmptyCache, attention.cpp:24-25).
+__device__ __forceinline__ float empty_guard(const DevState& s, float o, float l) {
+    if (l > 0.f) return o / l;
+    set_status(s.status, PE_EMPTY_CACHE);
+    return 0.f;
+}
+
 // Split-K completion: every split CTA of table i writes its partial, then
 // takes a ticket; the CTA holding the last ticket merges all splits
 // (out = sum_s o_s 2^(m_s - M) / sum_s l_s 2^(m_s - M)) and rearms the
@@ -63,7 +71,7 @@ __device__ __forceinline__ void merge_if_last(const DevState& s, const AttnArgs&
             ll += __ldcg(a.part_ml + pidx * 2 + 1) * c;
             oo += __ldcg(a.part_o + pidx * d + (x % d)) * c;
         }
-        a.out[((int64_t)seq * a.n_q_heads + h * G + g) * d + (x % d)] = oo / ll;
+        a.out[((int64_t)seq * a.n_q_heads + h * G + g) * d + (x % d)] = empty_guard(s, oo, ll);
     }
     if (threadIdx.x == 0) a.tickets[i] = 0;
 }
@@ -503,7 +511,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_mma_kernel(DevState
             oo += wpart_o[(w2 * G + gg) * D + (xi % D)] * c;
         }
         if (n_splits == 1) {  // the whole table: write the output directly
-            a.out[((int64_t)seq * a.n_q_heads + h * G + gg) * D + (xi % D)] = oo / ll;
+            a.out[((int64_t)seq * a.n_q_heads + h * G + gg) * D + (xi % D)] = empty_guard(s, oo, ll);
             continue;
         }
         const int64_t pidx = ((int64_t)i * n_splits + sp) * G + gg;
@@ -698,7 +706,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_tma_kernel(DevState
             oo += wpart_o[(w2 * G + gg) * D + (xi % D)] * c;
         }
         if (n_splits == 1) {
-            a.out[((int64_t)seq * a.n_q_heads + h * G + gg) * D + (xi % D)] = oo / ll;
+            a.out[((int64_t)seq * a.n_q_heads + h * G + gg) * D + (xi % D)] = empty_guard(s, oo, ll);
             continue;
         }
         const int64_t pidx = ((int64_t)i * n_splits + sp) * G + gg;

@@ -539,10 +539,6 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     }
     const int chunk_cap = (max_len + kPrefillCluster - 1) / kPrefillCluster;
     const size_t pack_smem = (size_t)chunk_cap * 12 + 16;  // keys + two u16 candidate lists
-    if (chunk_cap > 65535) return fail(PE_INVALID_ARG, "prefill length exceeds the select kernel's index range");
-    if (pack_smem > (size_t)e->max_dyn_prefill)
-        return fail(PE_INVALID_ARG, "prefill length " + std::to_string(max_len) +
-                                        " exceeds the per-cluster shared-memory capacity");
     const size_t tokens = cu_seqlens[n_seqs];
     const size_t in_bytes = tokens * (size_t)H * s.row_bytes;
     const uint8_t *dk = nullptr, *dv = nullptr;
@@ -596,6 +592,13 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     if (force_stream || force_cluster || (has_long && env_is(std::getenv("PE_SELECT_MIXED"), "0"))) max_short = 0;
     const bool long_cluster = force_cluster || env_is(std::getenv("PE_SELECT_LONG"), "cluster");
     const bool any_long = max_short == 0 || has_long;  // some table goes to the long-table kernel
+    if (any_long && long_cluster) {  // the cluster select holds a chunk of keys per CTA (u16 indices)
+        if (chunk_cap > 65535)
+            return fail(PE_INVALID_ARG, "prefill length exceeds the cluster select's index range");
+        if (pack_smem > (size_t)e->max_dyn_prefill)
+            return fail(PE_INVALID_ARG, "prefill length " + std::to_string(max_len) +
+                                            " exceeds the per-cluster shared-memory capacity");
+    }
     // the shared-memory select (and the fused variant built on it) holds a
     // whole table's high words per CTA; the cluster select a chunk per CTA
     const bool smem_capable = !has_long && !force_cluster && !force_stream;
@@ -1434,6 +1437,18 @@ pe_status pe_prompt_select(int32_t device, int32_t rule, const float* keys, int3
     if (ce == cudaSuccess) ce = cudaMemcpy(evicted_flags, flags, (size_t)n, cudaMemcpyDeviceToHost);
     release();
     if (ce != cudaSuccess) return fail(PE_CUDA_ERROR, std::string("prompt select: ") + cudaGetErrorString(ce));
+    return PE_OK;
+}
+
+pe_status pe_current_device(int32_t* device) {
+    if (device == nullptr) return fail(PE_INVALID_ARG, "null argument");
+    int ndev = 0, d = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(PE_NO_DEVICE, "no CUDA device");
+    }
+    PE_CUDA(cudaGetDevice(&d));
+    *device = d;
     return PE_OK;
 }
 

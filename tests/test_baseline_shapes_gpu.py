@@ -289,3 +289,21 @@ def test_cfg4_mixed_trace_shared_pool(reference):
     assert inv["pages_mapped"] + inv["free_pages"] == eng.capacity
     for (sq, h), sess in ref.items():
         np.testing.assert_array_equal(eng.retained_positions(sq * H + h), sess.read_table(0, False)["positions"])
+
+
+def test_prefill_longer_than_the_cluster_shared_memory():
+    """A 200 000-token prompt (beyond what the cluster select's shared memory
+    holds) goes through the streamed select: accepted and bit-exact."""
+    rng = np.random.default_rng(200000)
+    L, C, B, d = 200000, 4096, 16, 128
+    geo = pe.EngineGeometry(n_seqs=1, n_layers=1, n_kv_heads=1, head_dim=d, dtype=oracle.BF16)
+    eng = pe.PagedEvictionEngine(geo, pe.PolicyConfig(cache_budget=C, page_size=B))
+    orc = oracle.OracleEngine(n_seqs=1, n_layers=1, n_tab_heads=1, width=d, page_size=B, budget=C,
+                              dtype=oracle.BF16, capacity=eng.capacity, max_pages=eng.max_pages)
+    k, _ = random_kv(rng, (L, 1, d), oracle.BF16)
+    v, _ = random_kv(rng, (L, 1, d), oracle.BF16)
+    cu = np.array([0, L], np.int32)
+    ev = eng.prefill_compress(0, dev(k), dev(v), cu, evicted_counts=True)
+    _, oev = orc.prefill(0, k, v, cu)
+    np.testing.assert_array_equal(ev, oev)
+    compare_states_vectorized(eng.state(), oracle_state(orc), B, what="200K prefill: ")

@@ -365,6 +365,18 @@ def test_error_statuses():
     out = torch.empty((1, 3, 8), dtype=torch.float32, device="cuda")
     with pytest.raises(pe.LengthMismatch):
         eng2.attend(0, dev(np.ones((1, 3, 8), np.float32)), out, 3)
+    # attention over a table with no retained token -> EmptyCache (attention.cpp:24-25),
+    # output zeros instead of 0/0
+    geo = pe.EngineGeometry(n_seqs=2, n_layers=1, n_kv_heads=1, head_dim=64, dtype=oracle.BF16)
+    eng3 = pe.PagedEvictionEngine(geo, pe.PolicyConfig(cache_budget=16, page_size=16))
+    kb = np.tile(oracle.f32_to_bf16_bits(np.full(64, 0.25, np.float32)), (20, 1, 1))
+    eng3.prefill_compress(0, dev(kb), dev(kb), np.array([0, 20], np.int32), seq_begin=0)  # seq 1 stays empty
+    eng3.sync()
+    out3 = torch.full((2, 4, 64), 7.0, dtype=torch.float32, device="cuda")
+    eng3.attend(0, dev(np.zeros((2, 4, 64), np.uint16)), out3, 4)
+    with pytest.raises(pe.EmptyCache):
+        eng3.sync()
+    assert torch.all(out3[1] == 0) and torch.isfinite(out3).all()
 
 
 @pytest.mark.slow

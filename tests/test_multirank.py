@@ -1,9 +1,14 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2): sequences are sharded
-across ranks, each rank runs its own engine (here the C oracle engine, the
-CPU stand-in for the per-GPU CUDA engine) with its own pool and free list,
-and only the timing max and a stats struct cross ranks. The union of the
-ranks' decisions must equal a single-rank run over all sequences (tables
-are independent; only physical page ids differ, since pools differ)."""
+"""Multi-rank host logic (gloo, world_size 2): sequences are sharded across
+ranks, each rank runs its own engine with its own pool and free list, and
+only the timing max and a stats struct cross ranks. The union of the ranks'
+decisions must equal a single-rank run over all sequences (tables are
+independent; only physical page ids differ, since pools differ).
+
+Backends: the C oracle engine (CPU, runs everywhere) and the CUDA engine
+(`-m gpu`: two processes, each with its own engine on cuda:0, gloo between
+them — the single-GPU stand-in for one engine per GPU). The bench's own
+multi-rank path (`bench.py --gpus 2`, re-executed under torchrun) is run
+the same way with --share-device."""
 import os
 import socket
 
@@ -37,13 +42,47 @@ def inputs():
     return cu, pk, pv, dk, dv
 
 
-def run_shard(seq_lo, seq_hi):
+class _CudaShard:
+    """The CUDA engine behind the oracle engine's calls (same state readback)."""
+
+    def __init__(self, n):
+        import torch
+
+        import paper_2509_04377_b200 as pe
+
+        self.torch = torch
+        self.eng = pe.PagedEvictionEngine(
+            pe.EngineGeometry(n_seqs=n, n_layers=NL, n_kv_heads=H, head_dim=W, dtype=pe.DTYPE_F32, device=0),
+            pe.PolicyConfig(cache_budget=C, page_size=B))
+
+    def _d(self, a):
+        return self.torch.from_numpy(np.ascontiguousarray(a)).cuda(0)
+
+    def prefill(self, layer, k, v, cu):
+        self.eng.prefill_compress(layer, self._d(k), self._d(v), cu)
+        return (0,)
+
+    def decode(self, k, v, pos, step):
+        return self.eng.decode_step(0, NL, self._d(k), self._d(v), self._d(pos), step, victims=True)
+
+    def state(self):
+        bt, npg, nf, _ = self.eng.tables()
+        return bt, npg, nf, self.eng.positions()
+
+    def table_id(self, s, layer, h):
+        return self.eng.table_id(s, layer, h)
+
+
+def run_shard(seq_lo, seq_hi, backend="oracle"):
     """Runs sequences [seq_lo, seq_hi) on a private engine; returns per
     (global seq, layer, head) victims per step and final retained positions."""
     cu, pk, pv, dk, dv = inputs()
     n = seq_hi - seq_lo
-    eng = oracle.OracleEngine(n_seqs=n, n_layers=NL, n_tab_heads=H, width=W, page_size=B, budget=C,
-                              dtype=oracle.F32, capacity=n * NL * H * (C // B + 1), max_pages=C // B + 1)
+    if backend == "cuda":
+        eng = _CudaShard(n)
+    else:
+        eng = oracle.OracleEngine(n_seqs=n, n_layers=NL, n_tab_heads=H, width=W, page_size=B, budget=C,
+                                  dtype=oracle.F32, capacity=n * NL * H * (C // B + 1), max_pages=C // B + 1)
     lcu = (cu[seq_lo:seq_hi + 1] - cu[seq_lo]).astype(np.int32)
     for layer in range(NL):
         rows = slice(cu[seq_lo], cu[seq_hi])
@@ -52,8 +91,11 @@ def run_shard(seq_lo, seq_hi):
     victims = {}
     evicted = 0
     for st in range(STEPS):
-        assert eng.decode_append(0, NL, dk[st][:, seq_lo:seq_hi], dv[st][:, seq_lo:seq_hi], pos) == 0
-        _, vic = eng.decode_evict(0, NL)
+        if backend == "cuda":
+            vic = eng.decode(dk[st][:, seq_lo:seq_hi], dv[st][:, seq_lo:seq_hi], pos, st + 1)
+        else:
+            assert eng.decode_append(0, NL, dk[st][:, seq_lo:seq_hi], dv[st][:, seq_lo:seq_hi], pos) == 0
+            _, vic = eng.decode_evict(0, NL)
         i = 0
         for s in range(n):
             for layer in range(NL):
@@ -62,7 +104,10 @@ def run_shard(seq_lo, seq_hi):
                     evicted += vic[i] >= 0
                     i += 1
         pos += 1
-    bt, npg, nf, posn = eng.block_table(), eng.num_pages(), eng.newest_fill(), eng.positions()
+    if backend == "cuda":
+        bt, npg, nf, posn = eng.state()
+    else:
+        bt, npg, nf, posn = eng.block_table(), eng.num_pages(), eng.newest_fill(), eng.positions()
     retained = {}
     for s in range(n):
         for layer in range(NL):
@@ -73,11 +118,11 @@ def run_shard(seq_lo, seq_hi):
     return victims, retained, int(evicted)
 
 
-def worker(rank, world, port, q):
+def worker(rank, world, port, q, backend="oracle"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     lo, hi = shard(S, world, rank)
-    victims, retained, evicted = run_shard(lo, hi)
+    victims, retained, evicted = run_shard(lo, hi, backend)
     t = max_over_ranks(float(rank + 1))
     stats = gather_stats(RankStats(rank=rank, tables=(hi - lo) * NL * H, pages_evicted=evicted,
                                    kernel_ms=[1.0 + rank]))
@@ -99,11 +144,12 @@ def test_shard_partition():
             assert max(sizes) - min(sizes) <= 1
 
 
-def test_two_rank_gloo_equals_single_rank():
+@pytest.mark.parametrize("backend", ["oracle", pytest.param("cuda", marks=pytest.mark.gpu)])
+def test_two_rank_gloo_equals_single_rank(backend):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=worker, args=(r, 2, port, q, backend)) for r in range(2)]
     for p in procs:
         p.start()
     t, stats, gathered = q.get(timeout=240)
@@ -113,7 +159,7 @@ def test_two_rank_gloo_equals_single_rank():
     assert t == 2.0  # max over ranks
     assert [s["rank"] for s in stats] == [0, 1]
     assert sum(s["tables"] for s in stats) == S * NL * H
-    victims, retained, _ = run_shard(0, S)
+    victims, retained, _ = run_shard(0, S, backend)
     merged_v, merged_r = {}, {}
     for v, r in gathered:
         merged_v.update(v)
@@ -121,3 +167,68 @@ def test_two_rank_gloo_equals_single_rank():
     assert merged_v == victims
     assert merged_r == retained
     assert sum(s["pages_evicted"] for s in stats) == sum(1 for x in victims.values() if x >= 0)
+
+
+def _bench_line(out: str) -> dict:
+    import json
+
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_share_device():
+    """bench.py --gpus 2 re-executes itself under torch.distributed.run: two
+    ranks, each with its own engine and sequence shard (here both on cuda:0
+    with gloo, --share-device), one JSON line from rank 0 with n_gpus 2,
+    both ranks' stats, clean checks, and the whole-job value."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    res = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--share-device", "--config",
+                          "tiny", "--steps", "3", "--warmup", "3", "--no-cpu"], capture_output=True, text=True,
+                         timeout=600, env=env, cwd=root)
+    assert res.returncode == 0, res.stderr[-3000:]
+    line = _bench_line(res.stdout)
+    assert line["n_gpus"] == 2 and len(line["ranks"]) == 2
+    assert [r["rank"] for r in line["ranks"]] == [0, 1]
+    assert all(r["checks_ok"] for r in line["ranks"])
+    assert line["checks"]["cadence_ok"] and line["checks"]["invariant_violations"] == 0
+    assert line["config"]["tables_total"] == 2 * line["config"]["tables_per_gpu"]
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
+
+
+def test_bench_rejects_inconsistent_world():
+    """--gpus must match the launcher's WORLD_SIZE (no silent single rank)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    res = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "4"], capture_output=True, text=True,
+                         timeout=300, env=env, cwd=root)
+    assert res.returncode != 0 and "WORLD_SIZE=1" in res.stderr
+
+
+def test_bench_fails_loudly_without_enough_gpus():
+    """`bench.py --gpus 2` with fewer visible GPUs: the torchrun re-exec
+    starts two ranks and each refuses (no silent oversubscription)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    import torch
+
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("two GPUs visible")
+    root = Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    res = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--config", "tiny"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert res.returncode != 0
+    assert "needs 2 visible GPUs" in res.stderr + res.stdout
