@@ -8,8 +8,9 @@
 // streams and events. Prints one JSON line and exits non-zero if the device
 // invariant checker finds a violation.
 //
-// usage: decode_loop [seqs layers kv_heads head_dim prompt budget cycles]
-//        (defaults: BASELINE config 3 — 64 32 8 128 32768 4096 4)
+// usage: decode_loop [seqs layers kv_heads head_dim prompt budget cycles [score]]
+//        (defaults: BASELINE config 3 — 64 32 8 128 32768 4096 4; score:
+//        0 = PE_SCORE_RECOMPUTE (default), 1 = PE_SCORE_CACHED)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -64,7 +65,7 @@ void fill_bf16(void* dst, size_t bytes, uint64_t salt) {
 }  // namespace
 
 int main(int argc, char** argv) {
-    int S = 64, NL = 32, H = 8, d = 128, L = 32768, C = 4096, cycles = 4;
+    int S = 64, NL = 32, H = 8, d = 128, L = 32768, C = 4096, cycles = 4, score = PE_SCORE_RECOMPUTE;
     const int B = 16, G = 4;
     if (argc >= 8) {
         S = std::atoi(argv[1]);
@@ -75,6 +76,7 @@ int main(int argc, char** argv) {
         C = std::atoi(argv[6]);
         cycles = std::atoi(argv[7]);
     }
+    if (argc >= 9 && std::atoi(argv[8]) == 1) score = PE_SCORE_CACHED;
     pe_config cfg{};
     cfg.n_seqs = S;
     cfg.n_layers = NL;
@@ -143,7 +145,7 @@ int main(int argc, char** argv) {
             check(pe_decode_append(eng, 0, NL, static_cast<char*>(rk) + j * step_rows * row,
                                    static_cast<char*>(rv) + j * step_rows * row, pos + size_t(step) * S, st),
                   "append");
-        check(pe_decode_evict(eng, 0, NL, step, PE_SCORE_RECOMPUTE, nullptr, st), "evict");
+        check(pe_decode_evict(eng, 0, NL, step, static_cast<pe_score_mode>(score), nullptr, st), "evict");
     };
     cycle();  // warm-up
     cudaEventRecord(e0, st);

@@ -101,6 +101,27 @@ def build_metrics_fmt() -> tuple[Path, Path | None]:
     return b200, ref_out
 
 
+def build_acceptance() -> tuple[Path | None, Path | None]:
+    """acceptance_device.cpp (criteria 1-3, 6, 8 of the reference's acceptance
+    suite over the pagedevict:: API) against the façade
+    (tests/cpp/_build/acceptance_b200) and against the UNMODIFIED reference
+    sources (oracle/_ref/acceptance_ref). Needs the reference's test helpers
+    (tests/oracles.hpp, rng.hpp) at build time, so it is built only here."""
+    if not REF.exists():
+        return None, None
+    src = HERE / "acceptance_device.cpp"
+    b200 = _cxx([src], OUT / "acceptance_b200", [REF / "tests", REF / "core" / "include"], shim_main=False)
+    ref_dir = ROOT / "oracle" / "_ref"
+    ref_dir.mkdir(parents=True, exist_ok=True)
+    ref_out = ref_dir / "acceptance_ref"
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{REF / 'core' / 'include'}", f"-I{REF / 'tests'}", str(src),
+           *[str(REF / "core" / "src" / f) for f in REF_CORE], "-lpthread", "-o", str(ref_out)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"g++ failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stderr[-8000:]}")
+    return b200, ref_out
+
+
 def build_all() -> None:
     from paper_2509_04377_b200 import _build
 
@@ -109,6 +130,7 @@ def build_all() -> None:
     build_reference_conformance()
     build_scenario()
     build_metrics_fmt()
+    build_acceptance()
     build_examples()
 
 

@@ -105,3 +105,25 @@ def test_cpp_decode_loop_example():
     line = json.loads(res.stdout.strip().splitlines()[-1])
     assert line["invariant_violations"] == 0 and line["outputs_finite"] is True
     assert line["pages_evicted"] == 8 * 4 * 8 * 3
+
+
+@pytest.mark.gpu
+def test_acceptance_criteria_on_device():
+    """Acceptance criteria 1-3, 6 and 8 (acceptance_main.cpp:68-203,275-330,
+    361-367) through the façade on the B200: 100 scoring caches, 100 attention
+    instances, 1000 randomized budget/alignment traces (4 policies, B in
+    {8,16,32}, ~530K decode steps) and the StreamingLLM golden trace. Every
+    criterion passes, and the decision digests (every decision, retained
+    length, retained positions, page id and token score) equal those of the
+    same program built against the reference sources."""
+    ref = Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "acceptance_ref"
+    b200 = BUILD / "acceptance_b200"
+    if not ref.exists() or not b200.exists():
+        pytest.skip("acceptance binaries not built (tests/cpp/build_conformance.py)")
+    r = subprocess.run([str(ref)], capture_output=True, text=True, timeout=600)
+    g = subprocess.run([str(b200)], capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout + r.stderr[-2000:]
+    assert g.returncode == 0, g.stdout + g.stderr[-2000:]
+    assert "traces 1000" in g.stdout
+    assert g.stdout.count("PASS") == 5, g.stdout
+    assert g.stdout == r.stdout, (r.stdout, g.stdout)
