@@ -461,20 +461,23 @@ def run_b200(args, cfg, world, rank, local):
         if record is not None and not host and mode == pe.ScoreMode.RECOMPUTE:
             k0_evs[-1][1].record(stream)
         spans = [(0, NL)] if args.evict_launch == "step" else [(layer, 1) for layer in range(NL)]
+        # one event pair around the cycle's eviction launches: per-layer
+        # launches run back to back (consecutive K2 launches over disjoint
+        # layers overlap through programmatic dependent launch); each recorded
+        # entry is (start, end, launches) -> per-launch time = elapsed / launches
+        if record is not None:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if mode == pe.ScoreMode.CACHED:
+                # a ~50 us launch: keep the GPU busy so the event pair brackets
+                # device time, not the host's launch latency
+                torch.cuda._sleep(200_000)
+            a.record(stream)
         for l0, nl in spans:
-            vh = victims_host[: nl * n_tab_layer] if victims_host is not None else None
-            if record is not None:
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                if mode == pe.ScoreMode.CACHED:
-                    # a ~50 us launch: keep the GPU busy so the event pair brackets
-                    # device time, not the host's launch latency
-                    torch.cuda._sleep(200_000)
-                a.record(stream)
-                eng.evict(l0, nl, step=0, mode=mode, victims=vh)
-                b.record(stream)
-                record.append((a, b))
-            else:
-                eng.evict(l0, nl, step=0, mode=mode, victims=vh)
+            vh = victims_host[l0 * n_tab_layer: (l0 + nl) * n_tab_layer] if victims_host is not None else None
+            eng.evict(l0, nl, step=0, mode=mode, victims=vh)
+        if record is not None:
+            b.record(stream)
+            record.append((a, b, len(spans)))
 
     def barrier():
         if world > 1:
@@ -500,24 +503,24 @@ def run_b200(args, cfg, world, rank, local):
     ms_total = max_over_ranks(t0.elapsed_time(t1))
     ms_step = ms_total / args.steps
     total_step_bytes = sum_over_ranks(float(step_bytes))
-    k2_ms = [a.elapsed_time(b) for a, b in evs]
+    k2_ms = [a.elapsed_time(b) / n for a, b, n in evs]
     k2_mean = statistics.mean(k2_ms)
     value = total_step_bytes / (ms_step * 1e-3) / 1e9
     k2_gbs = k2_per_launch / (k2_mean * 1e-3) / 1e9
     # p50 evict-step µs over >= 100 trigger launches: extra
     # cycles after the timed region when --steps is smaller (not in `value`)
     evs_p50 = list(evs)
-    while len(evs_p50) < 100 * (1 if args.evict_launch == "step" else NL):
+    while sum(n for _, _, n in evs_p50) < 100 * (1 if args.evict_launch == "step" else NL):
         cycle(record=evs_p50)
     eng.sync()
-    k2_p50_ms = statistics.median(a.elapsed_time(b) for a, b in evs_p50)
+    k2_p50_ms = statistics.median(a.elapsed_time(b) / n for a, b, n in evs_p50)
 
     # ---------------- cached-score variant (K2c): p50 of the evict launch
     evc = []
     for _ in range(4):
         cycle(record=evc, mode=pe.ScoreMode.CACHED)
     eng.sync()
-    k2c_us = statistics.median([a.elapsed_time(b) * 1e3 for a, b in evc])
+    k2c_us = statistics.median([a.elapsed_time(b) * 1e3 / n for a, b, n in evc])
 
     # ---------------- the other launch granularity, for reference
     other = "layer" if args.evict_launch == "step" else "step"
@@ -528,7 +531,7 @@ def run_b200(args, cfg, world, rank, local):
         cycle(record=evo)
     eng.sync()
     args.evict_launch = saved
-    other_us = statistics.median([a.elapsed_time(b) * 1e3 for a, b in evo])
+    other_us = statistics.median([a.elapsed_time(b) * 1e3 / n for a, b, n in evo])
     other_bytes = (n_tab if other == "step" else n_tab_layer) * k2_bytes_per_table(C, row)
 
     # ---------------- e2e: host buffers through the C-ABI (recompute, then cached scores)
@@ -640,7 +643,7 @@ def run_b200(args, cfg, world, rank, local):
                        "parallelism": f"sequence-sharded x{world}, no data-path collective"},
             "pct_of_peak": round(100 * value / world / peak, 2),
             "p50_evict_step_us": round(k2_p50_ms * 1e3, 2),
-            "p50_evict_step_samples": len(evs_p50),
+            "p50_evict_step_samples": sum(n for _, _, n in evs_p50),
             "p50_evict_step_us_cached": round(k2c_us, 2),
             "append_us_per_launch_p50": round(statistics.median(a.elapsed_time(b) for a, b in k0_evs) * 1e3 / B, 2),
             "evict_launch": args.evict_launch,

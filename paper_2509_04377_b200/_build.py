@@ -23,7 +23,7 @@ LIB = LIB_DIR / "libpe_b200.so"
 FACADE_SRC = PKG / "cpp" / "pagedevict.cpp"
 FACADE_HDR = ROOT / "include" / "pe" / "pagedevict.hpp"
 FACADE_LIB = LIB_DIR / "libpagedevict_b200.so"
-SOURCES = ["pe_engine.cu", "pe_decode.cu", "pe_prefill.cu", "pe_attention.cu", "pe_table.cu"]
+SOURCES = ["pe_engine.cu", "pe_decode.cu", "pe_prefill.cu", "pe_select.cu", "pe_attention.cu", "pe_table.cu"]
 HEADERS = ["pe_internal.cuh", "pe_kernels.cuh", "pe_score.cuh", "pe_tma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

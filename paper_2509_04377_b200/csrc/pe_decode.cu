@@ -262,8 +262,10 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
 // free_page (retained -= fill; erase -> entries shift left, block_table.cpp:21-31).
 // The released page id is parked in vpage[i]; the grid's last CTA pushes all
 // of them on the free stack in ascending table id (push_victims below).
+// The released page id goes to *vslot (the launch's vpage entry of the
+// table), the logical victim to victims[i] (launch table i).
 __device__ __forceinline__ void finalize_evict(const DevState& s, int t, int i, int N, const double* scores,
-                                               int32_t* vpage, int32_t* victims) {
+                                               int32_t* vslot, int32_t* victims) {
     const int lane = threadIdx.x & 31;
     double best = 0.0;
     int bj = 0x7FFFFFFF;
@@ -286,11 +288,21 @@ __device__ __forceinline__ void finalize_evict(const DevState& s, int t, int i, 
     const int victim = bj;
     int32_t* row = s.block_table + (int64_t)t * s.max_pages;
     const int victim_page = row[victim];
-    // shift left in 32-entry chunks: every read of a chunk precedes its writes
-    for (int base = victim; base < N - 1; base += 32) {
-        const int v = (base + lane + 1 < N) ? row[base + lane + 1] : 0;
+    // shift left: up to 8 x 32 entries per round are loaded (independent
+    // loads, one round trip) before any of them is overwritten
+    for (int base = victim; base < N - 1; base += 8 * 32) {
+        int v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = base + u * 32 + lane + 1;
+            v[u] = j < N ? __ldcg(row + j) : 0;
+        }
         __syncwarp();
-        if (base + lane < N - 1) row[base + lane] = v;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = base + u * 32 + lane;
+            if (j < N - 1) row[j] = v[u];
+        }
         __syncwarp();
     }
     if (lane == 0) {
@@ -301,7 +313,7 @@ __device__ __forceinline__ void finalize_evict(const DevState& s, int t, int i, 
         s.retained[t] -= page_fill(s, victim_page, s.B);
         if (s.holes_on) s.holes[victim_page] = 0ull;
         s.newest_fill[t] = (N - 1 > 0) ? s.B : 0;
-        vpage[i] = victim_page;
+        *vslot = victim_page;
         if (victims) victims[i] = victim;
         atomicAdd(s.evict_count, 1ull);
     }
@@ -342,24 +354,34 @@ __device__ __forceinline__ double page_mean_b16(const DevState& s, int id, doubl
 
 // End of a K2 chunk: publish this CTA's page means, take the table's ticket;
 // the table's last CTA takes the argmin and evicts. Returns the tables settled.
+// scratch rows, tickets and vpage are indexed by TABLE id t (launch-
+// independent), so a programmatically overlapped next launch over other
+// tables never touches this launch's entries.
 __device__ __forceinline__ int publish_chunk(const DevState& s, int t, int y, int N, int p0, int np, int n_cta,
                                              const double* page_mean, double* scratch, int32_t* tickets,
                                              int32_t* vpage, int32_t* victims) {
     __shared__ int last;
     __syncthreads();
-    for (int j = threadIdx.x; j < np; j += blockDim.x) scratch[(int64_t)y * s.max_pages + p0 + j] = page_mean[j];
+    for (int j = threadIdx.x; j < np; j += blockDim.x) scratch[(int64_t)t * s.max_pages + p0 + j] = page_mean[j];
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = (atomicAdd(&tickets[y], 1) == n_cta - 1);
+    if (threadIdx.x == 0) last = (atomicAdd(&tickets[t], 1) == n_cta - 1);
     __syncthreads();
     if (!last) return 0;
     __threadfence();
     if ((threadIdx.x >> 5) == 0) {
-        finalize_evict(s, t, y, N, scratch + (int64_t)y * s.max_pages, vpage, victims);
-        if ((threadIdx.x & 31) == 0) tickets[y] = 0;
+        finalize_evict(s, t, y, N, scratch + (int64_t)t * s.max_pages, vpage + t, victims);
+        if ((threadIdx.x & 31) == 0) tickets[t] = 0;
     }
     return 1;
 }
+
+// Programmatic dependent launch (PDL) controls: a launch made with
+// programmatic stream serialization may start while the previous kernel of
+// the stream still runs; griddepcontrol.wait blocks until that kernel has
+// completed and its memory is visible (a no-op for a normal launch).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
 // evict_score_kernel (K2, recompute): grid (launch tables, chunks). CTA (y, c)
@@ -369,11 +391,23 @@ __device__ __forceinline__ int publish_chunk(const DevState& s, int t, int y, in
 // slot-order sum / fill (score_pages -> page_score, importance.cpp:19-39).
 // The last CTA of the table (atomic ticket) takes the argmin and evicts; the
 // last CTA of the grid pushes the released pages.
+//
+// early (PDL, per-layer launches back to back): the engine's previous launch
+// on this stream was a K2 launch over OTHER tables, so everything up to the
+// table's eviction touches state that launch never writes (this launch's
+// tables, their pages, their table-indexed scratch / ticket / vpage
+// entries); only the launch-level settle ticket and the free-stack push wait
+// for it. The next launch may start as soon as every CTA of this one has.
 template <int SV, bool HOLES>
 __global__ void __launch_bounds__(kEvictThreads, 5) evict_score_kernel(
     DevState s, TableSet ts, int pages_per_cta, double* scratch, int32_t* tickets, int32_t* vpage,
-    int32_t* victims, unsigned long long grid_last) {
+    int32_t* victims, unsigned long long grid_last, int early) {
     __shared__ double page_mean[kMaxPagesPerCta];
+    // not early: wait for the previous kernel BEFORE letting the next one
+    // start, so an early launch always starts after the last non-K2 kernel
+    // before the chain has completed
+    if (!early) pdl_wait();
+    pdl_launch_dependents();
     const int y = blockIdx.x;
     const int c = blockIdx.y;
     const int t = ts.table(s, y);
@@ -385,7 +419,7 @@ __global__ void __launch_bounds__(kEvictThreads, 5) evict_score_kernel(
         if (c == 0) {
             settled = 1;
             if (threadIdx.x == 0) {
-                vpage[y] = -1;
+                vpage[t] = -1;
                 if (victims) victims[y] = -1;
             }
         }
@@ -435,18 +469,39 @@ __global__ void __launch_bounds__(kEvictThreads, 5) evict_score_kernel(
         }
         settled = publish_chunk(s, t, y, N, p0, np, n_cta, page_mean, scratch, tickets, vpage, victims);
     }
-    push_victims_if_last(s, ts.size(s), vpage, grid_last, settled);
+    if (early) pdl_wait();  // the previous launch's settle tickets and pushes come first
+    push_victims_if_last(s, ts.size(s), vpage, grid_last, settled, &ts);
+}
+
+template <int SV, bool HOLES>
+void launch_evict_score_t(dim3 grid, int threads, cudaStream_t st, const DevState& s, const TableSet& ts, int ppc,
+                          double* scratch, int32_t* tickets, int32_t* vpage, int32_t* victims,
+                          unsigned long long grid_last, bool early) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = early ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, evict_score_kernel<SV, HOLES>, s, ts, ppc, scratch, tickets, vpage, victims, grid_last,
+                       early ? 1 : 0);
 }
 
 template <int SV>
 void launch_evict_score(dim3 grid, int threads, cudaStream_t st, const DevState& s, const TableSet& ts, int ppc,
                         double* scratch, int32_t* tickets, int32_t* vpage, int32_t* victims,
-                        unsigned long long grid_last) {
+                        unsigned long long grid_last, bool early) {
     // hole-aware variant only after the table API made holes (no runtime check in the hot loop)
     if (s.holes_on)
-        evict_score_kernel<SV, true><<<grid, threads, 0, st>>>(s, ts, ppc, scratch, tickets, vpage, victims, grid_last);
+        launch_evict_score_t<SV, true>(grid, threads, st, s, ts, ppc, scratch, tickets, vpage, victims, grid_last,
+                                       early);
     else
-        evict_score_kernel<SV, false><<<grid, threads, 0, st>>>(s, ts, ppc, scratch, tickets, vpage, victims, grid_last);
+        launch_evict_score_t<SV, false>(grid, threads, st, s, ts, ppc, scratch, tickets, vpage, victims, grid_last,
+                                        early);
 }
 
 template <int SV>
@@ -460,9 +515,9 @@ void launch_append(int blocks, cudaStream_t st, const DevState& s, const TableSe
 
 void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st, const DevState& s,
                             const TableSet& ts, int ppc, double* scratch, int32_t* tickets, int32_t* vpage,
-                            int32_t* victims, unsigned long long grid_last) {
+                            int32_t* victims, unsigned long long grid_last, bool early) {
     PE_SCORE_DISPATCH(variant, (launch_evict_score<SV>(grid, threads, st, s, ts, ppc, scratch, tickets, vpage,
-                                                        victims, grid_last)));
+                                                        victims, grid_last, early)));
 }
 
 void launch_append_any(int variant, int blocks, cudaStream_t st, const DevState& s, const TableSet& ts,
@@ -564,7 +619,7 @@ __global__ void __launch_bounds__(256) evict_cached_kernel(DevState s, TableSet 
             double* sc = scratch + (int64_t)y * s.max_pages;
             for (int j = lane; j < N; j += 32) sc[j] = s.page_scores[row[j]];
             __syncwarp();
-            finalize_evict(s, t, y, N, sc, vpage, victims);
+            finalize_evict(s, t, y, N, sc, vpage + y, victims);
         }
     }
     push_victims_if_last(s, n, vpage, grid_last, min(8, n - static_cast<int>(blockIdx.x) * 8));

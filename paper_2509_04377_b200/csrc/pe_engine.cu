@@ -77,6 +77,11 @@ struct pe_engine {
     bool append_chain = false;
     int32_t chain_layer0 = -1, chain_layers = 0;
     unsigned long long grid_tickets = 0;  // host mirror of DevState::grid_ctr
+    // K2 PDL chain: the engine's last launch was a recompute K2 over the
+    // contiguous layer range [k2_layer0, k2_layer0 + k2_layers) on k2_stream
+    bool k2_chain = false;
+    int32_t k2_layer0 = 0, k2_layers = 0;
+    cudaStream_t k2_stream = nullptr;
     double* evict_scratch = nullptr;
     int32_t* tab_len = nullptr;
     int64_t* tab_tok0 = nullptr;
@@ -88,6 +93,19 @@ struct pe_engine {
     size_t keys_elems = 0;
     int32_t* surv = nullptr;
     size_t surv_elems = 0;
+    // GPU-wide select scratch (pe_select.cu), sized per prefill call
+    uint2* gs_win = nullptr;
+    size_t gs_win_elems = 0;
+    int32_t* gs_tab = nullptr;  // cand_n and flag, [2][tables]
+    size_t gs_tab_elems = 0;
+    unsigned long long* gs_ckey = nullptr;
+    size_t gs_ckey_elems = 0;
+    int32_t* gs_cpos = nullptr;
+    size_t gs_cpos_elems = 0;
+    int32_t* gs_chunk = nullptr;
+    size_t gs_chunk_elems = 0;
+    uint32_t* gs_bits = nullptr;
+    size_t gs_bits_elems = 0;
     int variant = 0;
     int32_t* h_tab_len = nullptr;       // pinned
     int64_t* h_tab_tok0 = nullptr;      // pinned
@@ -110,6 +128,7 @@ struct pe_engine {
     cudaStream_t copy_stream = nullptr;
     cudaStream_t aux_stream = nullptr;   // second prefill wave stream
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_score = nullptr;      // prefill: the previous wave's score kernel is done (chained waves)
     cudaEvent_t ev_meta = nullptr;       // prefill metadata H2D copies done
     float* part_o = nullptr;
     size_t part_o_elems = 0;
@@ -213,9 +232,9 @@ void mark_consumed(pe_engine* e, cudaStream_t st) {
 int32_t elt_size(int32_t dtype) { return dtype == PE_DTYPE_BF16 ? 2 : 4; }
 
 pe_status check_launch(pe_engine* e, const char* what) {
+    if (e != nullptr) e->k2_chain = false;  // any other launch breaks the K2 PDL chain
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return fail(PE_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(err));
-    (void)e;
     return PE_OK;
 }
 
@@ -392,6 +411,7 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
         cudaStreamCreateWithFlags(&e->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_score, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_meta, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
         return cleanup_fail(fail(PE_CUDA_ERROR, "copy stream creation failed"));
@@ -420,6 +440,8 @@ pe_status pe_engine_create(const pe_config* cfg_in, pe_engine** out) {
             !allow(reinterpret_cast<const void*>(prefill_select_cta_kernel), &sel_cta) ||
             !allow(reinterpret_cast<const void*>(prefill_select_stream_kernel), &sel_cta) ||
             !allow(reinterpret_cast<const void*>(prefill_select_stream512_kernel), &sel_cta) ||
+            !allow(reinterpret_cast<const void*>(gsel_resolve_kernel), &sel_cta) ||
+            !allow(reinterpret_cast<const void*>(gsel_fallback_kernel), &sel_cta) ||
             !allow(prefill_fused_fn(e->variant), &sel_cta)) {
             cudaGetLastError();
             return cleanup_fail(fail(PE_CUDA_ERROR, "cudaFuncSetAttribute(max dynamic smem) failed"));
@@ -468,7 +490,8 @@ pe_status pe_engine_destroy(pe_engine* e) {
                    e->ctl, e->rank,
                    e->work, e->victims, e->tickets, e->evict_scratch, e->tab_len, e->tab_tok0,
                    e->tab_pagebase, e->evicted_dev, e->part_o,
-                   e->part_ml, e->out_stage, e->tab_keybase, e->keys, e->surv, e->lb_status,
+                   e->part_ml, e->out_stage, e->tab_keybase, e->keys, e->surv, e->gs_win, e->gs_tab, e->gs_ckey, e->gs_cpos,
+                   e->gs_chunk, e->gs_bits, e->lb_status,
                    e->alloc_out, e->tok_out, e->attn_tickets, e->items, e->seq_units, e->seq_done, e->work_ctr, e->attend_logits, e->attend_out, e->attend_ws, e->step_stage, e->tok_newest, e->tok_victims};
     for (void* p : dev) {
         if (p) cudaFree(p);
@@ -483,6 +506,7 @@ pe_status pe_engine_destroy(pe_engine* e) {
     if (e->aux_stream) cudaStreamDestroy(e->aux_stream);
     if (e->ev_fork) cudaEventDestroy(e->ev_fork);
     if (e->ev_join) cudaEventDestroy(e->ev_join);
+    if (e->ev_score) cudaEventDestroy(e->ev_score);
     if (e->ev_meta) cudaEventDestroy(e->ev_meta);
     if (e->h_tab_len) cudaFreeHost(e->h_tab_len);
     if (e->h_tab_tok0) cudaFreeHost(e->h_tab_tok0);
@@ -585,6 +609,13 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     // long-table kernel).
     const char* sel_env = std::getenv("PE_SELECT");
     auto env_is = [](const char* v, const char* x) { return v != nullptr && std::strcmp(v, x) == 0; };
+    // Default: the GPU-wide select (window / count / resolve / emit kernels,
+    // pe_select.cu) for tables of up to kGselMaxLen tokens. PE_SELECT=stream512
+    // restores the CTA-per-table selects below (the previous default).
+    const bool gsel_fb = env_is(sel_env, "global_fallback");  // test knob: the fallback for every table
+    const bool use_gsel = (sel_env == nullptr || env_is(sel_env, "global") || gsel_fb) &&
+                          !env_is(std::getenv("PE_SELECT_LONG"), "cluster") && max_len <= kGselMaxLen;
+    if (env_is(sel_env, "stream512")) sel_env = nullptr;
     const bool force_cluster = env_is(sel_env, "cluster");
     const bool force_stream = env_is(sel_env, "stream");
     const bool smem_short = env_is(sel_env, "smem");
@@ -687,6 +718,27 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
         PE_CUDA(cudaStreamWaitEvent(e->aux_stream, e->ev_fork, 0));
     }
     const int max_keep_pages = (std::min(max_len, s.policy == PE_POLICY_PAGED_EVICTION ? s.C : max_len) + s.B - 1) / s.B;
+    const bool chain = env_is(std::getenv("PE_PREFILL_CHAIN"), "1");
+    GselArgs gs{};
+    if (use_gsel) {
+        gs.cand_stride = std::min(kGselCandCap, max_len);
+        gs.chunk_stride = (max_len + kGselChunk - 1) / kGselChunk;
+        if ((r = ensure_t(&e->gs_win, &e->gs_win_elems, (size_t)n_tab)) != PE_OK ||
+            (r = ensure_t(&e->gs_tab, &e->gs_tab_elems, (size_t)2 * n_tab)) != PE_OK ||
+            (r = ensure_t(&e->gs_ckey, &e->gs_ckey_elems, (size_t)n_tab * gs.cand_stride)) != PE_OK ||
+            (r = ensure_t(&e->gs_cpos, &e->gs_cpos_elems, (size_t)n_tab * gs.cand_stride)) != PE_OK ||
+            (r = ensure_t(&e->gs_chunk, &e->gs_chunk_elems, (size_t)n_tab * gs.chunk_stride)) != PE_OK ||
+            (r = ensure_t(&e->gs_bits, &e->gs_bits_elems, (size_t)n_tab * gs.chunk_stride * kGselWords)) != PE_OK)
+            return r;
+        gs.win = e->gs_win;
+        gs.cand_n = e->gs_tab;
+        gs.flag = e->gs_tab + n_tab;
+        gs.cand_key = e->gs_ckey;
+        gs.cand_pos = e->gs_cpos;
+        gs.chunk_cnt = e->gs_chunk;
+        gs.evbits = e->gs_bits;
+        gs.force_fallback = gsel_fb ? 1 : 0;
+    }
     for (int w = 0; w < waves; ++w) {
         const int q0 = (int)((int64_t)n_seqs * w / waves);
         const int q1 = (int)((int64_t)n_seqs * (w + 1) / waves);
@@ -700,9 +752,28 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
         if (aw.evicted_counts) aw.evicted_counts += q0 * H;
         aw.seq_begin = seq_begin + q0;
         aw.n_tab = (q1 - q0) * H;
+        // chained waves: this wave's score starts when the previous wave's
+        // score is done, so that wave's select and copy run beside this score
+        if (chain && w > 0) PE_CUDA(cudaStreamWaitEvent(sw, e->ev_score, 0));
         launch_prefill_score_any(e->variant, dim3((max_len + aw.score_tokens - 1) / aw.score_tokens, q1 - q0),
                                  sw, s, aw, e->ctl);
-        if (max_short > 0) {  // tables of at most kSelectCtaMaxLen tokens
+        if (chain && w + 1 < waves) PE_CUDA(cudaEventRecord(e->ev_score, sw));
+        if (use_gsel) {
+            GselArgs gw = gs;
+            gw.tab_off = q0 * H;
+            const dim3 chunk_grid(aw.n_tab, gs.chunk_stride);
+            gsel_window_kernel<<<aw.n_tab, kGselSample, 0, sw>>>(s, aw, gw, e->ctl);
+            gsel_count_kernel<<<chunk_grid, 256, 0, sw>>>(s, aw, gw, e->ctl);
+            gsel_resolve_kernel<<<aw.n_tab, 512, kGselCandCap * 12, sw>>>(s, aw, gw, e->ctl);
+            // tables whose window missed: the streamed CTA-per-table select
+            PrefillArgs af = aw;
+            af.bits_cap = std::min((max_len + 31) / 32 * 32, kSelBitsMaxLen);
+            const size_t fb_smem = (size_t)kSelHistCopies * 2048 * 4 + (size_t)kSelCandCapStream * 4 +
+                                   (size_t)af.bits_cap / 8;
+            gsel_fallback_kernel<<<aw.n_tab, 1024, fb_smem, sw>>>(s, af, gw, e->ctl);
+            gsel_emit_kernel<<<chunk_grid, 64, 0, sw>>>(s, aw, gw, e->ctl);
+            e->stats.kernel_launches += 5;
+        } else if (max_short > 0) {  // tables of at most kSelectCtaMaxLen tokens
             PrefillArgs ac = aw;
             ac.cta_len_max = kSelectCtaMaxLen;
             if (smem_short) {
@@ -712,19 +783,24 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
                 prefill_select_cta_kernel<<<aw.n_tab, 1024, sel_smem, sw>>>(s, ac, e->ctl);
             } else {
                 ac.cand_cap = kSelCandCap;
-                const size_t smem5 = (size_t)kSelHistCopies * 2048 * 4 + (size_t)kSelCandCap * 4;
+                ac.bits_cap = (kSelectCtaMaxLen + 31) / 32 * 32;  // eviction bitmap: 4.3 KB
+                const size_t smem5 =
+                    (size_t)kSelHistCopies * 2048 * 4 + (size_t)kSelCandCap * 4 + (size_t)ac.bits_cap / 8;
                 prefill_select_stream512_kernel<<<aw.n_tab, 512, smem5, sw>>>(s, ac, e->ctl);
             }
             e->stats.kernel_launches += 1;
         }
-        if (any_long) {  // the longer tables (every table when max_short == 0)
+        if (any_long && !use_gsel) {  // the longer tables (every table when max_short == 0)
             PrefillArgs al = aw;
             al.cluster_len_min = max_short > 0 ? kSelectCtaMaxLen : -1;
             if (long_cluster) {
                 prefill_select_kernel<<<dim3(kPrefillCluster, aw.n_tab), kPackThreads, pack_smem, sw>>>(s, al,
                                                                                                      e->ctl);
             } else {
-                const size_t st_smem = (size_t)kSelHistCopies * 2048 * 4 + (size_t)kSelCandCapStream * 4;
+                // eviction bitmap for tables up to kSelBitsMaxLen tokens (longer: the sweeps)
+                al.bits_cap = std::min((max_len + 31) / 32 * 32, kSelBitsMaxLen);
+                const size_t st_smem = (size_t)kSelHistCopies * 2048 * 4 + (size_t)kSelCandCapStream * 4 +
+                                       (size_t)al.bits_cap / 8;
                 prefill_select_stream_kernel<<<aw.n_tab, 1024, st_smem, sw>>>(s, al, e->ctl);
             }
             e->stats.kernel_launches += 1;
@@ -762,6 +838,14 @@ pe_status launch_evict(pe_engine* e, const DevState& sc, const TableSet& ts, int
     int32_t* vdst = vic_dev ? victims : e->victims;
     // one launch: the grid's last CTA pushes the released pages in ascending
     // table id (no separate planner)
+    // PDL (programmatic dependent launch): a recompute launch right after one
+    // over a disjoint layer range of the same engine on the same stream
+    // scores and evicts while that launch drains (evict_score_kernel `early`)
+    const char* pdl_env = std::getenv("PE_K2_PDL");  // A/B: 0 = plain stream order
+    const bool early = mode == PE_SCORE_RECOMPUTE && !(pdl_env != nullptr && std::strcmp(pdl_env, "0") == 0) &&
+                       e->k2_chain && e->k2_stream == st && ts.ids == nullptr &&
+                       (ts.layer_begin >= e->k2_layer0 + e->k2_layers ||
+                        ts.layer_begin + ts.n_layers <= e->k2_layer0);
     if (mode == PE_SCORE_RECOMPUTE) {
         // Pages per CTA: as many as possible (a CTA's warps stream their pages
         // without draining; one CTA per table reaches 97 % of the HBM peak on
@@ -779,7 +863,7 @@ pe_status launch_evict(pe_engine* e, const DevState& sc, const TableSet& ts, int
         chunks = (sc.max_pages + ppc - 1) / ppc;
         e->grid_tickets += (unsigned long long)n;  // one completion ticket per table
         launch_evict_score_any(e->variant, dim3(n, chunks), kEvictThreads, st, sc, ts, ppc,
-                               e->evict_scratch, e->tickets, e->vpage, vdst, e->grid_tickets - 1);
+                               e->evict_scratch, e->tickets, e->vpage, vdst, e->grid_tickets - 1, early);
     } else {
         e->grid_tickets += (unsigned long long)n;
         evict_cached_kernel<<<(n + 7) / 8, 256, 0, st>>>(sc, ts, e->evict_scratch, e->vpage, vdst,
@@ -787,6 +871,12 @@ pe_status launch_evict(pe_engine* e, const DevState& sc, const TableSet& ts, int
     }
     pe_status r = check_launch(e, "evict kernel");
     if (r != PE_OK) return r;
+    if (mode == PE_SCORE_RECOMPUTE && ts.ids == nullptr) {
+        e->k2_chain = true;
+        e->k2_layer0 = ts.layer_begin;
+        e->k2_layers = ts.n_layers;
+        e->k2_stream = st;
+    }
     e->stats.kernel_launches += 1;
     e->stats.evict_calls += 1;
     if (victims && !vic_dev) {

@@ -190,8 +190,11 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sm, int* total) {
 // released pages on the free stack in ascending table id (release,
 // page_pool.cpp:35-38; canonical order DESIGN.md §1.6). `settled` is
 // block-uniform.
+// by_table (K2 recompute): vpage is indexed by table id, launch table i's
+// entry is vpage[by_table->table(s, i)].
 __device__ __forceinline__ void push_victims_if_last(const DevState& s, int n, int32_t* vpage,
-                                                     unsigned long long grid_last, int settled) {
+                                                     unsigned long long grid_last, int settled,
+                                                     const TableSet* by_table = nullptr) {
     __shared__ int is_last;
     __shared__ int scan_sm[33];
     __threadfence();
@@ -210,7 +213,7 @@ __device__ __forceinline__ void push_victims_if_last(const DevState& s, int n, i
         int cnt = 0;
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
-            v[u] = (i0 + u < n) ? __ldcg(vpage + i0 + u) : -1;
+            v[u] = (i0 + u < n) ? __ldcg(vpage + (by_table ? by_table->table(s, i0 + u) : i0 + u)) : -1;
             cnt += v[u] >= 0;
         }
         int total;

@@ -33,6 +33,7 @@ struct PrefillArgs {
     int32_t cta_len_max;                 // CTA select: tables longer than this are skipped
     int32_t cluster_len_min;             // cluster select: tables this short or shorter are skipped
     int32_t cand_cap;                    // streamed select: candidate list capacity (shared memory)
+    int32_t bits_cap;                    // streamed select: eviction bitmap capacity in positions (0 = none)
 };
 
 __global__ void evict_cached_kernel(DevState s, TableSet ts, double* scratch, int32_t* vpage, int32_t* victims,
@@ -44,7 +45,35 @@ constexpr int kSelHistCopies = 8;        // private histogram copies in the CTA 
 constexpr int kSelCandCap = 4096;        // boundary-bin candidates compacted after the first radix pass
 constexpr int kSelectCtaMaxLen = 34816;  // CTA-per-table select: 4 B of smem per token + 64 KB histograms + 16 KB candidates
 constexpr int kSelCandCapStream = 16384;  // candidates of the streamed CTA select (no hi words in smem)
+constexpr int kSelBitsMaxLen = 262144;    // streamed select: eviction bitmap (32 KB) for tables up to this length
 __global__ void prefill_select_stream_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
+
+// GPU-wide select (pe_select.cu): window / count / resolve / emit kernels
+constexpr int kGselChunk = 2048;                    // positions per count / emit CTA
+constexpr int kGselWords = kGselChunk / 32;         // eviction-bit words per chunk
+constexpr int kGselSample = 1024;                   // sampled high words per table (window)
+constexpr int kGselAll = 4096;                      // tables this short: every key is a candidate
+constexpr int kGselCandCap = 8192;                  // candidates sorted in shared memory (96 KB)
+constexpr int kGselMaxChunks = 128;                 // tables up to 128 chunks (262144 tokens)
+constexpr int kGselMaxLen = kGselChunk * kGselMaxChunks;
+constexpr int kGselMaxTies = 1024;                  // keys equal to the threshold resolved in the resolve kernel
+struct GselArgs {
+    uint2* win;                          // [tables] high-word window (inclusive)
+    int32_t* cand_n;                     // [tables] candidates appended
+    unsigned long long* cand_key;        // [tables][cand_stride]
+    int32_t* cand_pos;                   // [tables][cand_stride]
+    int32_t* chunk_cnt;                  // [tables][chunk_stride] below counts, then survivor bases
+    uint32_t* evbits;                    // [tables][chunk_stride][kGselWords] eviction bits
+    int32_t* flag;                       // [tables] 1: the window missed, CTA-per-table select
+    int32_t tab_off;                     // call-level index of the wave's first table
+    int32_t cand_stride, chunk_stride;
+    int32_t force_fallback;              // test knob (PE_SELECT=global_fallback)
+};
+__global__ void gsel_window_kernel(DevState s, PrefillArgs a, GselArgs g, const LaunchCtl* ctl);
+__global__ void gsel_count_kernel(DevState s, PrefillArgs a, GselArgs g, const LaunchCtl* ctl);
+__global__ void gsel_resolve_kernel(DevState s, PrefillArgs a, GselArgs g, const LaunchCtl* ctl);
+__global__ void gsel_emit_kernel(DevState s, PrefillArgs a, GselArgs g, const LaunchCtl* ctl);
+__global__ void gsel_fallback_kernel(DevState s, PrefillArgs a, GselArgs g, const LaunchCtl* ctl);
 __global__ void prefill_select_stream512_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 __global__ void prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 // persistent fused prefill (score units + per-table select/copy), pe_prefill.cu
@@ -60,7 +89,7 @@ void launch_append_any(int variant, int blocks, cudaStream_t st, const DevState&
                        LaunchCtl* ctl, unsigned long long ticket_base, int epoch, bool fast_ok);
 void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st, const DevState& s,
                             const TableSet& ts, int ppc, double* scratch, int32_t* tickets, int32_t* vpage,
-                            int32_t* victims, unsigned long long grid_last);
+                            int32_t* victims, unsigned long long grid_last, bool early);
 void launch_prefill_score_any(int variant, dim3 grid, cudaStream_t st, const DevState& s, const PrefillArgs& a,
                               const LaunchCtl* ctl);
 

@@ -508,6 +508,10 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
         reinterpret_cast<uint32_t*>(SMEM_HI ? smem + (((size_t)a.chunk_cap * 4 + 15) & ~size_t(15)) : smem);
     uint32_t* my_hist = hcopy + ((threadIdx.x >> 5) % kSelHistCopies) * 2048;
     int32_t* cand = reinterpret_cast<int32_t*>(hcopy + kSelHistCopies * 2048);  // [cand_cap]
+    // streamed select: one eviction bit per position (after the candidates)
+    // when the table fits a.bits_cap — the windowed path then classifies and
+    // emits from shared memory instead of re-reading every key
+    uint32_t* evbits = reinterpret_cast<uint32_t*>(cand + cand_cap);
     const unsigned long long* gk = a.keys + a.tab_keybase[i];
     auto HI = [&](int j) -> uint32_t {
         if constexpr (SMEM_HI) return hi[j];
@@ -521,6 +525,7 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
     // key falls inside the window (the common case), the radix passes visit
     // only the candidates; otherwise the plain full-table passes run.
     const bool sampled = E > 0 && L >= 8192;
+    const bool bits = !SMEM_HI && sampled && L <= a.bits_cap;
     unsigned int p_lo = 0u, p_hi = 0xFFFFFFFFu;
     uint32_t* seg = hcopy;  // per-warp candidate segments during the load
     constexpr int kSegCap = kSelHistCopies * 2048 / 32;
@@ -583,6 +588,12 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
                 hmax = max(hmax, w);
             }
             if (sampled) {
+                if (bits) {
+                    // below-window keys are evicted: one bitmap word per 32
+                    // positions (spans are 32-aligned, lane = position % 32)
+                    const unsigned bm = __ballot_sync(0xFFFFFFFFu, in && w < p_lo);
+                    if (lane_id == 0 && j0 + u * 32 < w_end) evbits[(j0 + u * 32) >> 5] = bm;
+                }
                 n_below += in && w < p_lo;
                 const bool c = in && w >= p_lo && w <= p_hi;
                 const unsigned m = __ballot_sync(0xFFFFFFFFu, c);
@@ -769,6 +780,55 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
             }
         }
     };
+    if (windowed && bits) {
+        // the bitmap holds the below-window evictions; the candidates (in
+        // ascending position order: warp segments in warp order) add theirs,
+        // ties by tie rank in position order (importance.cpp:46-52)
+        int tie_run = 0;
+        for (int x0 = 0; x0 < n_cand; x0 += nthr) {
+            const int x = x0 + tid;
+            bool l = false, t = false;
+            int j = 0;
+            if (x < n_cand) {
+                j = cand[x];
+                classify(j, l, t);
+            }
+            int n_tie;
+            const int tr = tie_run + block_excl_scan(t ? 1 : 0, scan_sm, &n_tie);
+            if (l || (t && tr < k_rem)) atomicOr(&evbits[j >> 5], 1u << (j & 31));
+            tie_run += n_tie;
+        }
+        __syncthreads();
+        // survivors per warp span (lane-parallel over the span's words)
+        int kc = 0;
+        for (int b = w_beg + lane_id * 32; b < w_end; b += 32 * 32) {
+            const int nv = min(32, w_end - b);
+            const unsigned valid = nv == 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
+            kc += __popc(~evbits[b >> 5] & valid);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) kc += __shfl_xor_sync(0xFFFFFFFFu, kc, o);
+        if (lane_id == 0) w_keepb[warp_id] = kc;
+        __syncthreads();
+        if (tid == 0) {
+            int run = 0;
+            for (int w = 0; w < (nthr >> 5); ++w) {
+                const int c = w_keepb[w];
+                w_keepb[w] = run;
+                run += c;
+            }
+        }
+        __syncthreads();
+        int keep_run = w_keepb[warp_id];
+        const unsigned lt = (1u << lane_id) - 1u;
+        for (int b = w_beg; b < w_end; b += 32) {
+            const int p = b + lane_id;
+            const bool kp = p < w_end && !((evbits[b >> 5] >> lane_id) & 1u);
+            const unsigned kb = __ballot_sync(0xFFFFFFFFu, kp);
+            if (kp) surv[keep_run + __popc(kb & lt)] = p;
+            keep_run += __popc(kb);
+        }
+    } else {
     if (windowed) {
         // per-warp (less, tie) counts without a counting sweep: the load pass
         // counted each warp's keys below the window; only the candidates need
@@ -792,6 +852,7 @@ __device__ __noinline__ void select_table_cta(const DevState& s, const PrefillAr
     if (tid == 0) sweep_bases(L, k_rem, 0, 0, w_less, w_tie, w_tieb, w_keepb);
     __syncthreads();
     sweep_emit(L, classify, k_rem, w_tieb, w_keepb, [&](int q, int j) { surv[q] = j; });
+    }
     // ---- 4. table metadata
     const int n_pages = (keep + B - 1) / B;
     const int pop_base = ctl->pop_base;
@@ -834,6 +895,17 @@ __global__ void __launch_bounds__(512, 2) prefill_select_stream512_kernel(DevSta
     if (ctl->abort) return;
     const int L = a.tab_len[blockIdx.x];
     if (L <= a.cluster_len_min || L > a.cta_len_max) return;  // the other select kernel's table
+    select_table_cta<false>(s, a, blockIdx.x, smem, ctl);
+}
+
+// The global select's fallback (pe_select.cu): tables whose sampled window
+// missed the boundary (tie-heavy or adversarial score distributions) take the
+// streamed CTA-per-table select; every other CTA exits at once.
+__global__ void __launch_bounds__(1024, 1) gsel_fallback_kernel(DevState s, PrefillArgs a, GselArgs g,
+                                                                const LaunchCtl* ctl) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    if (ctl->abort) return;
+    if (!g.flag[g.tab_off + blockIdx.x]) return;
     select_table_cta<false>(s, a, blockIdx.x, smem, ctl);
 }
 

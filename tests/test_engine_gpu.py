@@ -49,11 +49,13 @@ def check(eng, orc, what="", pages=True):
                 assert st["page_scores"][pid] == ost["page_scores"][pid], f"{what}page score {pid}"
 
 
-@pytest.fixture(params=["default", "smem", "stream", "cluster"])
+@pytest.fixture(params=["default", "global_fallback", "stream512", "smem", "stream", "cluster"])
 def select_path(request, monkeypatch):
-    """Run prefill through every select kernel: the default 512-thread
-    streamed CTA select, the shared-memory CTA select, the 1024-thread
-    streamed select and the 8-CTA cluster select."""
+    """Run prefill through every select kernel: the default GPU-wide select
+    (window / count / resolve / emit, pe_select.cu), its fallback forced for
+    every table (PE_SELECT=global_fallback), the 512-thread streamed
+    CTA select, the shared-memory CTA select, the 1024-thread streamed
+    select and the 8-CTA cluster select."""
     if request.param == "default":
         monkeypatch.delenv("PE_SELECT", raising=False)
     else:
@@ -103,16 +105,18 @@ def prefill_variant(request, monkeypatch):
     return request.param
 
 
-@pytest.mark.parametrize("sel", ["default", "smem"])
+@pytest.mark.parametrize("sel", ["default", "global_fallback", "stream512", "smem"])
 @pytest.mark.parametrize("gen", [random_kv, grid_kv])
 def test_prefill_long_tables_windowed_select(gen, prefill_variant, sel, monkeypatch):
-    """Tables of >= 8192 tokens take the sampled pivot window of the CTA
-    select kernel (candidates only; tie-heavy grid data overflows the window
-    and exercises the full-pass fallback). Bit-exact against the oracle."""
-    if sel == "smem":
-        monkeypatch.setenv("PE_SELECT", "smem")
-    else:
+    """Tables of >= 8192 tokens take the sampled pivot window (the GPU-wide
+    select's window kernel, or the CTA selects'); tie-heavy grid data
+    overflows the window and exercises the fallbacks (the CTA-per-table
+    select behind the global select, the full passes inside the CTA
+    selects). Bit-exact against the oracle."""
+    if sel == "default":
         monkeypatch.delenv("PE_SELECT", raising=False)
+    else:
+        monkeypatch.setenv("PE_SELECT", sel)
     rng = np.random.default_rng(8192)
     B, C, d, H = 16, 2048, 128, 2
     lens = np.array([8192, 32768, 20001, 9000, 4096 + 1])
@@ -129,8 +133,12 @@ def test_prefill_long_tables_windowed_select(gen, prefill_variant, sel, monkeypa
 
 
 @pytest.mark.parametrize("dtype", [oracle.F32, oracle.BF16])
-@pytest.mark.parametrize("mode", [0, 1])
-def test_decode_parity(dtype, mode):
+@pytest.mark.parametrize("mode,k2", [(0, "flat"), (0, "grid"), (1, "cached")])
+def test_decode_parity(dtype, mode, k2, monkeypatch):
+    """K0 + K2 (recompute: the flat persistent kernel of small launches, or
+    the (table, chunk) grid with PE_K2_FLAT=0) or K2c, all-layer and
+    per-layer launches, bit-exact against the oracle."""
+    monkeypatch.setenv("PE_K2_FLAT", "0" if k2 == "grid" else "1")
     rng = np.random.default_rng(7 + 10 * dtype + mode)
     B, C, H, n_layers, S = 16, 64, 2, 3, 3
     d = 64 if dtype == oracle.F32 else 128
@@ -146,7 +154,19 @@ def test_decode_parity(dtype, mode):
     for step in range(1, 3 * B + 4):
         k, _ = random_kv(rng, (n_layers, S, H, d), dtype)
         v, _ = random_kv(rng, (n_layers, S, H, d), dtype)
-        if step % 3 == 0:  # per-layer launches
+        if step % 3 == 1 and mode == 0:
+            # one append over all layers, then per-layer evictions back to
+            # back with device-side victims (no host copy in between: the K2
+            # launches chain through programmatic dependent launch)
+            eng.append_token(0, n_layers, dev(k), dev(v), dev(pos))
+            assert orc.decode_append(0, n_layers, k, v, pos) == 0
+            vics = [torch.full((S * H,), -7, dtype=torch.int32, device="cuda") for _ in range(n_layers)]
+            for layer in range(n_layers):
+                eng.evict(layer, 1, step=step, mode=mode, victims=vics[layer])
+            for layer in range(n_layers):
+                _, ovic = orc.decode_evict(layer, 1)
+                np.testing.assert_array_equal(vics[layer].cpu().numpy(), ovic, err_msg=f"step {step} layer {layer}")
+        elif step % 3 == 0:  # per-layer launches
             for layer in range(n_layers):
                 vic = eng.decode_step(layer, 1, dev(k[layer:layer + 1]), dev(v[layer:layer + 1]),
                                       dev(pos), step, mode=mode, victims=True)
@@ -166,6 +186,46 @@ def test_decode_parity(dtype, mode):
     eng.sync()
     check(eng, orc, "final: ")
     assert eng.stats().pages_evicted > 0
+
+
+@pytest.mark.parametrize("pdl", ["1", "0"])
+def test_per_layer_evictions_back_to_back(pdl, monkeypatch):
+    """Per-layer K2 launches issued back to back on one stream (a serving
+    loop's eviction of every layer): with PE_K2_PDL=1 each launch after the
+    first overlaps its predecessor (programmatic dependent launch: scoring
+    and table eviction before griddepcontrol.wait, the free-stack push after).
+    16 x 4 x 8 = 512 tables of C + B = 1040 tokens, 9 chunks per table;
+    victims, block tables, positions, page bytes and the free list bit-exact
+    against the oracle after every cycle, the pushes in launch order."""
+    monkeypatch.setenv("PE_K2_PDL", pdl)
+    rng = np.random.default_rng(4096)
+    B, C, H, n_layers, S, d = 16, 1024, 8, 4, 16, 128
+    lens = np.full(S, 2048)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=S, n_layers=n_layers, H=H, d=d, B=B, C=C, dtype=oracle.BF16)
+    for layer in range(n_layers):
+        k, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+        v, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+        eng.prefill_compress(layer, dev(k), dev(v), cu)
+        orc.prefill(layer, k, v, cu)
+    pos = lens.astype(np.int64).copy()
+    for cycle in range(3):
+        for j in range(B):
+            k, _ = random_kv(rng, (n_layers, S, H, d), oracle.BF16)
+            v, _ = random_kv(rng, (n_layers, S, H, d), oracle.BF16)
+            eng.append_token(0, n_layers, dev(k), dev(v), dev(pos))
+            assert orc.decode_append(0, n_layers, k, v, pos) == 0
+            pos += 1
+        vics = [torch.full((S * H,), -7, dtype=torch.int32, device="cuda") for _ in range(n_layers)]
+        for layer in range(n_layers):
+            eng.evict(layer, 1, step=(cycle + 1) * B, victims=vics[layer])
+        for layer in range(n_layers):
+            _, ovic = orc.decode_evict(layer, 1)
+            np.testing.assert_array_equal(vics[layer].cpu().numpy(), ovic, err_msg=f"cycle {cycle} layer {layer}")
+        eng.sync()
+        st = eng.state(with_pages=(cycle == 2))
+        compare_states_vectorized(st, oracle_state(orc), B, check_pages=(cycle == 2), what=f"cycle {cycle}: ")
+    assert eng.stats().pages_evicted == 3 * S * n_layers * H
 
 
 @pytest.mark.parametrize("fast", ["1", "0"])

@@ -28,11 +28,15 @@ ROOT = Path(__file__).resolve().parent.parent
 BINARY = ROOT / "tests" / "cpp" / "_build" / "decode_loop"
 
 # seqs layers kv_heads head_dim prompt budget cycles [score]: 40 x 8 x 8 =
-# 2560 tables = 40 K0 CTAs (two look-back groups), 1024-token prompts, C=256
-SMALL = ["40", "8", "8", "128", "1024", "256", "2"]
+# 2560 tables = 40 K0 CTAs (two look-back groups); 8192-token prompts with
+# C=1024 take the sampled-window select (bitmap emit), 1024-token prompts
+# with C=256 the full radix passes and position sweeps
+SMALL = ["40", "8", "8", "128", "8192", "1024", "2"]
+SHORT = ["40", "8", "8", "128", "1024", "256", "2"]
 
 VARIANTS = {
     "default": ({}, SMALL),
+    "short_prompts": ({}, SHORT),
     "cached_score": ({}, SMALL + ["1"]),
     "select_smem": ({"PE_SELECT": "smem"}, SMALL),
     "select_cluster": ({"PE_SELECT": "cluster"}, SMALL),
@@ -44,8 +48,9 @@ VARIANTS = {
 
 TOOL_VARIANTS = {
     "memcheck": list(VARIANTS),
-    "racecheck": ["default", "select_smem", "select_cluster", "attn_splits4_cpasync"],
-    "synccheck": ["default", "select_cluster", "attn_splits4_cpasync"],
+    "racecheck": ["default", "short_prompts", "select_smem", "select_stream1024", "select_cluster",
+                  "attn_splits4_cpasync"],
+    "synccheck": ["default", "short_prompts", "select_cluster", "attn_splits4_cpasync"],
 }
 
 

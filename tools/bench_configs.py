@@ -130,6 +130,14 @@ def run(name, layers, kvh, d, qh, lens, C, dtype, decode_steps, waves=1, pool_la
     torch.cuda.synchronize()
     all_ms = [a.elapsed_time(b) for a, b in all_ms]
     evicted = eng.stats().pages_evicted - evicted0
+    # checks (untimed): the device invariant checker over the whole state and
+    # the eviction cadence — a table that starts decode at R0 = min(L, C)
+    # retained tokens has made max(0, floor((R0 + D) / B) - C / B) page
+    # evictions after D decode tokens (policy.cpp:147-150; pages never have
+    # holes, so the newest page is full exactly when retained % B == 0)
+    D = decode_steps + B
+    expect = layers * kvh * sum(max(0, (min(L, C) + D) // B - C // B) for L in lens)
+    inv = eng.check_invariants()
     # eviction launches at a trigger step (all tables of the layer triggered together in uniform configs)
     trig = [a.elapsed_time(b) for a, b in k2_ms]
     _, _, _, retained = eng.tables()
@@ -145,6 +153,9 @@ def run(name, layers, kvh, d, qh, lens, C, dtype, decode_steps, waves=1, pool_la
         "evict_nontrigger_step_us_p50": round(statistics.median([a.elapsed_time(b) for a, b in k2_other]) * 1e3, 2),
         "evict_cached_us_p50": round(statistics.median([a.elapsed_time(b) for a, b in k2c_ms]) * 1e3, 2),
         "pages_evicted": int(evicted),
+        "checks": {"evictions_expected": int(expect), "evictions_observed": int(evicted),
+                   "cadence_ok": int(expect) == int(evicted), "invariant_violations": int(inv["violations"]),
+                   "tables_checked": n_tab},
         "attention": {"us_p50": round(statistics.median(k3) * 1e3, 2),
                       "gbs": round(k3_bytes / (statistics.median(k3) * 1e-3) / 1e9, 1),
                       "mean_retained": round(mean_R, 1)},
