@@ -416,7 +416,7 @@ def run_b200(args, cfg, world, rank, local):
     n_tab_layer = S * H
     k1_bytes = n_tab_layer * k1_bytes_per_table(L, C, row)
     pre_p50 = statistics.median(pre_ms[1:] or pre_ms)
-    prefill = {"kernel": "K1 prefill_prune_pack: score + CTA-per-table select + copy, "
+    prefill = {"kernel": "K1 prefill_prune_pack: score + GPU-wide select (window/count/resolve/emit) + rescoring copy, "
                          "2 sequence waves on 2 streams",
                "ms_per_layer_p50": round(pre_p50, 4),
                "gbs": round(k1_bytes / (pre_p50 * 1e-3) / 1e9, 1),

@@ -770,7 +770,10 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
             af.bits_cap = std::min((max_len + 31) / 32 * 32, kSelBitsMaxLen);
             const size_t fb_smem = (size_t)kSelHistCopies * 2048 * 4 + (size_t)kSelCandCapStream * 4 +
                                    (size_t)af.bits_cap / 8;
-            gsel_fallback_kernel<<<aw.n_tab, 1024, fb_smem, sw>>>(s, af, gw, e->ctl);
+            // strided over the wave's tables (only flagged ones do work)
+            int fb_grid = std::min(aw.n_tab, e->sm_count);
+            if (const char* fg = std::getenv("PE_FB_GRID")) fb_grid = std::max(1, std::min(aw.n_tab, std::atoi(fg)));
+            gsel_fallback_kernel<<<fb_grid, 1024, fb_smem, sw>>>(s, af, gw, e->ctl);
             gsel_emit_kernel<<<chunk_grid, 64, 0, sw>>>(s, aw, gw, e->ctl);
             e->stats.kernel_launches += 5;
         } else if (max_short > 0) {  // tables of at most kSelectCtaMaxLen tokens
@@ -805,7 +808,7 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
             }
             e->stats.kernel_launches += 1;
         }
-        prefill_copy_kernel<<<dim3(aw.n_tab, (max_keep_pages + 3) / 4), 128, 0, sw>>>(s, aw, e->ctl);
+        launch_prefill_copy_any(e->variant, dim3(aw.n_tab, (max_keep_pages + 3) / 4), sw, s, aw, e->ctl);
         e->stats.kernel_launches += 2;  // score + copy (the selects counted above)
     }
     if (waves > 1) {
@@ -849,13 +852,15 @@ pe_status launch_evict(pe_engine* e, const DevState& sc, const TableSet& ts, int
     if (mode == PE_SCORE_RECOMPUTE) {
         // Pages per CTA: as many as possible (a CTA's warps stream their pages
         // without draining; one CTA per table reaches 97 % of the HBM peak on
-        // an all-layer launch), but enough CTAs for ~6 waves on small launches
-        // (a per-layer launch of 512 tables gets 9 chunks of 29 pages).
+        // an all-layer launch), but at least ~3 CTAs per SM on small launches
+        // (cfg2's per-layer launch of 256 tables: 2 chunks of 65 pages; cfg3's
+        // 512 tables: one CTA per table). With per-layer launches chained by
+        // PDL the next launch fills the SMs a launch's tail leaves idle, so
+        // fewer, longer CTAs win: cfg3 per-layer 195 -> 171 us (28 -> 3 CTAs
+        // per SM target), cfg2 65 -> 45 us (tools/k2_ab.py).
         const int min_chunks = (sc.max_pages + kMaxPagesPerCta - 1) / kMaxPagesPerCta;
-        static const int ctas_per_sm = [] {
-            const char* v = std::getenv("PE_K2_CTAS_PER_SM");  // tuning override
-            return v ? std::max(1, std::atoi(v)) : 28;
-        }();
+        const char* cps_env = std::getenv("PE_K2_CTAS_PER_SM");  // tuning override (read per call: A/B)
+        const int ctas_per_sm = cps_env ? std::max(1, std::atoi(cps_env)) : 3;
         const int target_ctas = ctas_per_sm * e->sm_count;
         int chunks = std::max(min_chunks, (target_ctas + n - 1) / n);
         chunks = std::max(min_chunks, std::min(chunks, (sc.max_pages + 7) / 8));

@@ -12,6 +12,7 @@ constexpr int kEvictThreads = 128;       // 4 warps per CTA
 constexpr int kMaxPagesPerCta = 288;
 constexpr int kPrefillThreads = 128;     // score kernel: 4 warps per CTA
 constexpr int kScoreTokensPerCta = 64;   // tokens (x all heads) per score CTA (small CTAs balance best)
+constexpr int kScoreKeysMax = 1024;      // score CTA: keys staged in shared memory (8 KB)
 constexpr int kPackThreads = 256;        // select kernel: 8 warps per CTA
 constexpr int kPrefillCluster = 8;       // CTAs per table (portable cluster size)
 
@@ -74,8 +75,43 @@ __global__ void gsel_count_kernel(DevState s, PrefillArgs a, GselArgs g, const L
 __global__ void gsel_resolve_kernel(DevState s, PrefillArgs a, GselArgs g, const LaunchCtl* ctl);
 __global__ void gsel_emit_kernel(DevState s, PrefillArgs a, GselArgs g, const LaunchCtl* ctl);
 __global__ void gsel_fallback_kernel(DevState s, PrefillArgs a, GselArgs g, const LaunchCtl* ctl);
+// The window from a strided sample of high words, one per thread of a
+// kGselSample-thread CTA (both window kernels): bitonic sort (partner
+// distances >= 32 through shared memory, shorter ones as warp shuffles),
+// then the sample's boundary rank E*kGselSample/L +- 3.5 binomial sigma.
+// The window holds the E-th key with overwhelming probability; the resolve
+// kernel checks it exactly.
+__device__ __forceinline__ uint2 gsel_window_of_sample(uint32_t x, uint32_t* samp, int E, int L) {
+    const int tid = threadIdx.x;
+    for (int k = 2; k <= kGselSample; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const bool up = (tid & k) == 0;
+            const bool lower = (tid & j) == 0;
+            uint32_t y;
+            if (j >= 32) {
+                samp[tid] = x;
+                __syncthreads();
+                y = samp[tid ^ j];
+                __syncthreads();
+            } else {
+                y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+            }
+            x = (lower == up) ? min(x, y) : max(x, y);
+        }
+    }
+    samp[tid] = x;
+    __syncthreads();
+    const double p = static_cast<double>(E) / L;
+    const int win = static_cast<int>(ceil(3.5 * sqrt(kGselSample * p * (1.0 - p)))) + 4;
+    const int r = static_cast<int>(((int64_t)E * kGselSample) / L);
+    const int lo = r - win, hi = r + win;
+    return make_uint2(lo <= 0 ? 0u : samp[lo], hi >= kGselSample - 1 ? 0xFFFFFFFFu : samp[hi]);
+}
 __global__ void prefill_select_stream512_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 __global__ void prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
+// the copy (PE_COPY_RESCORE=1: survivors rescored from the copied registers)
+void launch_prefill_copy_any(int variant, dim3 grid, cudaStream_t st, const DevState& s, const PrefillArgs& a,
+                             const LaunchCtl* ctl);
 // persistent fused prefill (score units + per-table select/copy), pe_prefill.cu
 void launch_prefill_fused_any(int variant, int grid, size_t smem, cudaStream_t st, const DevState& s,
                               const PrefillArgs& a, const LaunchCtl* ctl, const int32_t* items, int n_items,

@@ -30,6 +30,8 @@
 //               by plan_prefill_kernel. Token scores and positions are stored
 //               beside the page; full pages get their mean score cached.
 #include <cooperative_groups.h>
+#include <cstdlib>
+#include <cstring>
 
 #include "pe_kernels.cuh"
 #include "pe_score.cuh"
@@ -73,9 +75,15 @@ __global__ void __launch_bounds__(1024) plan_prefill_kernel(DevState s, PrefillA
 // (token, head) rows of a token block are one contiguous span and every
 // warp step (16 lane pairs = 16 consecutive (token, head) rows of K and of
 // V) reads 4 KB of contiguous HBM.
-template <int SV>
+//
+// SK (staged keys, a.score_tokens * heads <= kScoreKeysMax): the CTA's keys
+// are gathered in shared memory and written per table as one contiguous run
+// of score_tokens keys (full 32-byte sectors) instead of 2-key pieces from
+// each warp step.
+template <int SV, bool SK>
 __global__ void __launch_bounds__(kPrefillThreads) prefill_score_kernel(DevState s, PrefillArgs a,
                                                                          const LaunchCtl* ctl) {
+    __shared__ unsigned long long skeys[SK ? kScoreKeysMax : 1];
     if (ctl->abort) return;
     const int sq = blockIdx.y;  // sequence within the launch
     const int H = s.tab_heads;
@@ -96,16 +104,33 @@ __global__ void __launch_bounds__(kPrefillThreads) prefill_score_kernel(DevState
         const int64_t off = (row0 + f) * s.row_bytes;
         const double S = pair_token_score<SV>(a.k + off, a.v + off, valid, s.w, s.dtype);
         if (valid && (lane & 1) == 0) {
-            const int tok = static_cast<int>(f / H);
-            const int h = static_cast<int>(f - (int64_t)tok * H);
-            a.keys[a.tab_keybase[sq * H + h] + tok] = static_cast<unsigned long long>(__double_as_longlong(S));
+            const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(S));
+            if constexpr (SK) {
+                skeys[f - f_lo] = key;  // (token, head) order
+            } else {
+                const int tok = static_cast<int>(f / H);
+                const int h = static_cast<int>(f - (int64_t)tok * H);
+                a.keys[a.tab_keybase[sq * H + h] + tok] = key;
+            }
+        }
+    }
+    if constexpr (SK) {
+        __syncthreads();
+        const int nt = tok_hi - tok_lo;
+        for (int x = threadIdx.x; x < nt * H; x += blockDim.x) {  // head-major: one run per table
+            const int h = x / nt, j = x - h * nt;
+            a.keys[a.tab_keybase[sq * H + h] + tok_lo + j] = skeys[j * H + h];
         }
     }
 }
 
 template <int SV>
 static void launch_score(dim3 grid, cudaStream_t st, const DevState& s, const PrefillArgs& a, const LaunchCtl* ctl) {
-    prefill_score_kernel<SV><<<grid, kPrefillThreads, 0, st>>>(s, a, ctl);
+    const char* sk = std::getenv("PE_SCORE_STAGED_KEYS");
+    if ((int64_t)a.score_tokens * s.tab_heads <= kScoreKeysMax && !(sk != nullptr && std::strcmp(sk, "0") == 0))
+        prefill_score_kernel<SV, true><<<grid, kPrefillThreads, 0, st>>>(s, a, ctl);
+    else
+        prefill_score_kernel<SV, false><<<grid, kPrefillThreads, 0, st>>>(s, a, ctl);
 }
 
 void launch_prefill_score_any(int variant, dim3 grid, cudaStream_t st, const DevState& s, const PrefillArgs& a,
@@ -905,8 +930,12 @@ __global__ void __launch_bounds__(1024, 1) gsel_fallback_kernel(DevState s, Pref
                                                                 const LaunchCtl* ctl) {
     extern __shared__ __align__(16) uint8_t smem[];
     if (ctl->abort) return;
-    if (!g.flag[g.tab_off + blockIdx.x]) return;
-    select_table_cta<false>(s, a, blockIdx.x, smem, ctl);
+    for (int i = blockIdx.x; i < a.n_tab; i += gridDim.x) {
+        if (g.flag[g.tab_off + i]) {  // block-uniform
+            select_table_cta<false>(s, a, i, smem, ctl);
+            __syncthreads();
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -969,6 +998,57 @@ __device__ __forceinline__ void copy_page_warp(const DevState& s, const PrefillA
 __global__ void __launch_bounds__(128) prefill_copy_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
     if (ctl->abort) return;
     copy_page_warp(s, a, ctl, blockIdx.x, blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5));
+}
+
+// The same packing with each survivor's S recomputed from the row registers
+// it is copied from (pair_token_score with destinations: every load of the
+// row is issued before its stores, and no key is gathered): the score is the
+// same function of the same bytes, so it is bit-identical to the key.
+template <int SV>
+__global__ void __launch_bounds__(128) prefill_copy_score_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
+    if (ctl->abort) return;
+    const int i = blockIdx.x;
+    const int j = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int L = a.tab_len[i];
+    const int keep = (s.policy == PE_POLICY_PAGED_EVICTION && L > s.C) ? s.C : L;
+    const int B = s.B;
+    const int n_pages = (keep + B - 1) / B;
+    if (j >= n_pages) return;
+    const int h = i % s.tab_heads;
+    const int64_t row0 = (a.tab_tok0[i] * s.tab_heads + h) * (int64_t)s.row_bytes;
+    const int pagebase = a.tab_pagebase[i];
+    const int page = s.stack[ctl->pop_base - 1 - (pagebase + j)];
+    const int32_t* surv = a.surv + (int64_t)pagebase * B;
+    double sum = 0.0;
+    for (int s0 = 0; s0 < B; s0 += 16) {
+        const int slot = s0 + (lane >> 1);
+        const int q = j * B + slot;
+        const bool valid = slot < B && q < keep;
+        const int tok = valid ? __ldg(surv + q) : 0;
+        const int64_t src = row0 + (int64_t)tok * a.token_stride;
+        uint8_t* kd = s.pages + (((int64_t)page * 2 + 0) * B + slot) * s.pitch;
+        uint8_t* vd = s.pages + (((int64_t)page * 2 + 1) * B + slot) * s.pitch;
+        const double S = pair_token_score<SV>(a.k + src, a.v + src, valid, s.w, s.dtype, kd, vd);
+        if (valid && (lane & 1) == 0) {
+            s.positions[(int64_t)page * B + slot] = tok;
+            s.token_scores[(int64_t)page * B + slot] = S;
+        }
+        const int ns = min(16, B - s0);
+        for (int u = 0; u < ns; ++u) sum += __shfl_sync(0xFFFFFFFFu, S, 2 * u);
+    }
+    if (lane == 0 && (j + 1) * B <= keep) s.page_scores[page] = sum / static_cast<double>(B);
+}
+
+void launch_prefill_copy_any(int variant, dim3 grid, cudaStream_t st, const DevState& s, const PrefillArgs& a,
+                             const LaunchCtl* ctl) {
+    const char* rs = std::getenv("PE_COPY_RESCORE");  // A/B: 0 = gather the keys (prefill_copy_kernel)
+    const bool rescore = !(rs != nullptr && std::strcmp(rs, "0") == 0) && s.pitch == s.row_bytes;
+    if (rescore) {
+        PE_SCORE_DISPATCH(variant, (prefill_copy_score_kernel<SV><<<grid, 128, 0, st>>>(s, a, ctl)));
+    } else {
+        prefill_copy_kernel<<<grid, 128, 0, st>>>(s, a, ctl);
+    }
 }
 
 // ---------------------------------------------------------------------------

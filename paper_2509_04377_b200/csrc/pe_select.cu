@@ -48,35 +48,9 @@ __global__ void __launch_bounds__(kGselSample) gsel_window_kernel(DevState s, Pr
     const int E = L - table_keep(s, L);
     uint2 w = make_uint2(0u, 0xFFFFFFFFu);  // short tables: every key is a candidate
     if (E > 0 && L > kGselAll) {
-        // one strided sample per thread; bitonic sort with partner distances
-        // >= 32 through shared memory and shorter ones as warp shuffles
         const unsigned long long* gk = a.keys + a.tab_keybase[i];
-        uint32_t x = static_cast<uint32_t>(__ldcg(gk + (int)(((int64_t)tid * L) / kGselSample)) >> 32);
-        for (int k = 2; k <= kGselSample; k <<= 1) {
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                const bool up = (tid & k) == 0;
-                const bool lower = (tid & j) == 0;
-                uint32_t y;
-                if (j >= 32) {
-                    samp[tid] = x;
-                    __syncthreads();
-                    y = samp[tid ^ j];
-                    __syncthreads();
-                } else {
-                    y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
-                }
-                x = (lower == up) ? min(x, y) : max(x, y);
-            }
-        }
-        samp[tid] = x;
-        __syncthreads();
-        // rank of the boundary in the sample and a +-3.5 sigma binomial margin
-        const double p = static_cast<double>(E) / L;
-        const int win = static_cast<int>(ceil(3.5 * sqrt(kGselSample * p * (1.0 - p)))) + 4;
-        const int r = static_cast<int>(((int64_t)E * kGselSample) / L);
-        const int lo = r - win, hi = r + win;
-        w.x = lo <= 0 ? 0u : samp[lo];
-        w.y = hi >= kGselSample - 1 ? 0xFFFFFFFFu : samp[hi];
+        const uint32_t x = static_cast<uint32_t>(__ldcg(gk + (int)(((int64_t)tid * L) / kGselSample)) >> 32);
+        w = gsel_window_of_sample(x, samp, E, L);
     }
     if (tid == 0) {
         g.win[gi] = w;

@@ -82,6 +82,36 @@ def test_prefill_parity(dtype, gen, select_path):
     check(eng, orc, "prefill: ")
 
 
+@pytest.mark.parametrize("variant", ["copy_gather", "unstaged_keys", "fallback_grid2"])
+@pytest.mark.parametrize("dtype", [oracle.F32, oracle.BF16])
+@pytest.mark.parametrize("gen", [random_kv, grid_kv])
+def test_prefill_kernel_variants(variant, dtype, gen, monkeypatch):
+    """The K1 A/B paths beside the defaults: the copy that gathers each
+    survivor's key instead of rescoring its row (PE_COPY_RESCORE=0), per-warp
+    key stores instead of the CTA-staged runs (PE_SCORE_STAGED_KEYS=0), and
+    the global select's fallback looping over a wave's flagged tables with 2
+    CTAs (PE_FB_GRID=2, every table flagged). Bit-exact against the oracle."""
+    env = {"copy_gather": {"PE_COPY_RESCORE": "0"},
+           "unstaged_keys": {"PE_SCORE_STAGED_KEYS": "0"},
+           "fallback_grid2": {"PE_FB_GRID": "2", "PE_SELECT": "global_fallback"}}[variant]
+    monkeypatch.delenv("PE_SELECT", raising=False)
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    rng = np.random.default_rng(300 + dtype)
+    B, C, d, H = 16, 512, 64 if dtype == oracle.F32 else 128, 2
+    lens = np.array([C + 1, 9000, C, 5, 3 * C + 7, 4097])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=len(lens), n_layers=1, H=H, d=d, B=B, C=C, dtype=dtype)
+    k, _ = gen(rng, (cu[-1], H, d), dtype)
+    v, _ = gen(rng, (cu[-1], H, d), dtype)
+    ev = eng.prefill_compress(0, dev(k), dev(v), cu, evicted_counts=True)
+    st, oev = orc.prefill(0, k, v, cu)
+    assert st == 0
+    np.testing.assert_array_equal(ev, oev)
+    eng.sync()
+    check(eng, orc, f"{variant}: ")
+
+
 def test_prefill_ties_across_cta_boundaries(select_path):
     """Every token of a table scores identically: the E evicted tokens must be
     exactly the oldest E (position tie rule, importance.cpp:46-52), even
