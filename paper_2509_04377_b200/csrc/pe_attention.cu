@@ -348,6 +348,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_mma_kernel(DevState
     constexpr int NT = D / 8;          // PV n-tiles
     constexpr int PIECES = RB / 16;
     extern __shared__ __align__(16) uint8_t smem[];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see attention_tma_kernel
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
@@ -559,6 +560,8 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_tma_kernel(DevState
     extern __shared__ __align__(16) uint8_t smem[];  // aligned to 1024 B by hand (align1024)
     __shared__ __align__(8) uint64_t bars[kAttnThreads / 32][NST];
     __shared__ int32_t ids[kAttnMaxSplitPages];
+    // a K2 launch over another layer may start early behind this one (PDL)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;

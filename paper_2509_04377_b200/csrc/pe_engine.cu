@@ -77,8 +77,9 @@ struct pe_engine {
     bool append_chain = false;
     int32_t chain_layer0 = -1, chain_layers = 0;
     unsigned long long grid_tickets = 0;  // host mirror of DevState::grid_ctr
-    // K2 PDL chain: the engine's last launch was a recompute K2 over the
-    // contiguous layer range [k2_layer0, k2_layer0 + k2_layers) on k2_stream
+    // K2 PDL chain: the engine's last launch was a recompute K2 (or a
+    // tensor-core attention) over the contiguous layer range
+    // [k2_layer0, k2_layer0 + k2_layers) on k2_stream
     bool k2_chain = false;
     int32_t k2_layer0 = 0, k2_layers = 0;
     cudaStream_t k2_stream = nullptr;
@@ -1073,6 +1074,16 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
     mark_consumed(e, st);
     r = check_launch(e, "attention");
     if (r != PE_OK) return r;
+    if (use_mma) {
+        // the tensor-core attention writes only its partials, tickets and
+        // output: a recompute K2 over another layer may follow it through PDL
+        // (decode order attend(l) -> evict(l + 1): the eviction streams its
+        // pages while this launch drains)
+        e->k2_chain = true;
+        e->k2_layer0 = layer;
+        e->k2_layers = 1;
+        e->k2_stream = st;
+    }
     e->stats.kernel_launches += 1;
     e->stats.attention_calls += 1;
     if (!out_dev) {

@@ -258,6 +258,54 @@ def test_per_layer_evictions_back_to_back(pdl, monkeypatch):
     assert eng.stats().pages_evicted == 3 * S * n_layers * H
 
 
+@pytest.mark.parametrize("pdl", ["1", "0"])
+def test_serving_order_evict_attend_interleaved(pdl, monkeypatch):
+    """A serving loop's per-layer order: append on every layer, then per
+    layer evict(l) -> attend(l). With PE_K2_PDL=1 each evict(l + 1) launches
+    behind attend(l) through programmatic dependent launch (the attention
+    writes only its own partials and output; the eviction of another layer's
+    tables streams while it drains). Victims of every layer and the GQA
+    outputs (bf16 tolerance 1e-3) against the oracle at every step; the whole
+    state bit-exact at the end."""
+    monkeypatch.setenv("PE_K2_PDL", pdl)
+    rng = np.random.default_rng(5150)
+    B, C, H, G, n_layers, S, d = 16, 512, 4, 4, 3, 8, 128
+    lens = np.full(S, 1200)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=S, n_layers=n_layers, H=H, d=d, B=B, C=C, dtype=oracle.BF16)
+    for layer in range(n_layers):
+        k, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+        v, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+        eng.prefill_compress(layer, dev(k), dev(v), cu)
+        orc.prefill(layer, k, v, cu)
+    pos = lens.astype(np.int64).copy()
+    for step in range(1, 2 * B + 3):
+        k, _ = random_kv(rng, (n_layers, S, H, d), oracle.BF16)
+        v, _ = random_kv(rng, (n_layers, S, H, d), oracle.BF16)
+        eng.append_token(0, n_layers, dev(k), dev(v), dev(pos))
+        assert orc.decode_append(0, n_layers, k, v, pos) == 0
+        pos += 1
+        q, _ = random_kv(rng, (n_layers, S, H * G, d), oracle.BF16)
+        outs, vics = [], []
+        for layer in range(n_layers):
+            vics.append(torch.full((S * H,), -7, dtype=torch.int32, device="cuda"))
+            eng.evict(layer, 1, step=step, victims=vics[-1])
+            outs.append(torch.empty((S, H * G, d), dtype=torch.float32, device="cuda"))
+            eng.attend(layer, dev(np.ascontiguousarray(q[layer])), outs[-1], H * G)
+        for layer in range(n_layers):
+            _, ovic = orc.decode_evict(layer, 1)
+            np.testing.assert_array_equal(vics[layer].cpu().numpy(), ovic, err_msg=f"step {step} layer {layer}")
+            _, ref = orc.attention(layer, np.ascontiguousarray(q[layer]), G)
+            got = outs[layer].cpu().numpy()
+            for s_ in range(S):
+                for hq in range(H * G):
+                    dv = oracle.Oracle().output_deviation(got[s_, hq], ref[s_, hq])
+                    assert dv <= 1e-3, f"step {step} layer {layer} seq {s_} head {hq}: deviation {dv}"
+    eng.sync()
+    check(eng, orc, "serving order: ")
+    assert eng.stats().pages_evicted == 2 * S * n_layers * H
+
+
 @pytest.mark.parametrize("fast", ["1", "0"])
 def test_append_chain_parity(fast, monkeypatch):
     """Runs of consecutive appends (the K0 no-pop fast path: the previous

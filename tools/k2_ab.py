@@ -35,7 +35,9 @@ B = 16
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
-    ap.add_argument("--launch", default="layer", choices=["layer", "step"])
+    ap.add_argument("--launch", default="layer", choices=["layer", "step", "serve"],
+                    help="serve: per decode token, append on every layer, then per layer evict(l) + attend(l) "
+                         "(GQA, 4 query heads per KV head); the time is per decode token")
     ap.add_argument("--cycles", type=int, default=12)
     ap.add_argument("--variant", action="append", required=True, help="name:VAR=val,VAR=val")
     args = ap.parse_args()
@@ -67,18 +69,36 @@ def main():
     per_table = (C + B) * row + 8 * (C // B + 1) + 4
     n_tab = S * NL * H
     spans = [(0, NL)] if args.launch == "step" else [(ly, 1) for ly in range(NL)]
+    G = 4
+    q = torch.randn((S, H * G, d), generator=gen, device="cuda").to(torch.bfloat16)
+    out = torch.empty((S, H * G, d), dtype=torch.float32, device="cuda")
     launch_bytes = per_table * (n_tab if args.launch == "step" else S * H)
     times = {n: [] for n, _ in variants}
     pos = L
     for c in range(args.cycles + 1):
         for name, env in variants:
+            for kk in keys:
+                os.environ.pop(kk, None)
+            os.environ.update(env)
+            if args.launch == "serve":
+                ps = [torch.full((S,), pos + j, dtype=torch.int64, device="cuda") for j in range(B)]
+                pos += B
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for j in range(B):
+                    eng.append_token(0, NL, rows_k[j], rows_v[j], ps[j])
+                    for ly in range(NL):
+                        eng.evict(ly, 1, step=j + 1)
+                        eng.attend(ly, q, out, H * G)
+                b.record(stream)
+                b.synchronize()
+                if c > 0:
+                    times[name].append(a.elapsed_time(b) / B)
+                continue
             for j in range(B):
                 p = torch.full((S,), pos, dtype=torch.int64, device="cuda")
                 eng.append_token(0, NL, rows_k[j], rows_v[j], p)
                 pos += 1
-            for kk in keys:
-                os.environ.pop(kk, None)
-            os.environ.update(env)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             for l0, nl in spans:
@@ -91,14 +111,16 @@ def main():
         os.environ.pop(kk, None)
     eng.sync()
     inv = eng.check_invariants()
-    out = {"config": args.config, "launch": args.launch, "bytes_per_launch": launch_bytes, "invariants": inv,
+    res = {"config": args.config, "launch": args.launch, "bytes_per_launch": launch_bytes, "invariants": inv,
            "variants": {}}
     for name, env in variants:
         ms = statistics.median(times[name])
-        out["variants"][name] = {"env": env, "us_per_launch_p50": round(ms * 1e3, 2),
+        res["variants"][name] = {"env": env, "us_per_launch_p50": round(ms * 1e3, 2),
                                  "us_all": [round(x * 1e3, 1) for x in times[name]],
                                  "gbs": round(launch_bytes / (ms * 1e-3) / 1e9, 1)}
-    print(json.dumps(out))
+        if args.launch == "serve":
+            res["variants"][name]["tokens_per_s"] = round(S / (ms * 1e-3), 1)
+    print(json.dumps(res))
 
 
 if __name__ == "__main__":
