@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_mma_kernel(DevState
     constexpr int NT = D / 8;          // PV n-tiles
     constexpr int PIECES = RB / 16;
     extern __shared__ __align__(16) uint8_t smem[];
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see attention_tma_kernel
+    pdl_top();  // see attention_tma_kernel
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
@@ -531,8 +531,8 @@ size_t attention_mma_smem(int d, int G) {
 }
 
 void launch_attention_mma(int d, dim3 grid, size_t smem, cudaStream_t st, const DevState& s, const AttnArgs& a) {
-    if (d == 128) attention_mma_kernel<128><<<grid, kAttnThreads, smem, st>>>(s, a);
-    else attention_mma_kernel<64><<<grid, kAttnThreads, smem, st>>>(s, a);
+    if (d == 128) launch_pdl(attention_mma_kernel<128>, grid, dim3(kAttnThreads), smem, st, s, a);
+    else launch_pdl(attention_mma_kernel<64>, grid, dim3(kAttnThreads), smem, st, s, a);
 }
 
 const void* attention_mma_fn(int d) {
@@ -560,8 +560,9 @@ __global__ void __launch_bounds__(kAttnThreads, 2) attention_tma_kernel(DevState
     extern __shared__ __align__(16) uint8_t smem[];  // aligned to 1024 B by hand (align1024)
     __shared__ __align__(8) uint64_t bars[kAttnThreads / 32][NST];
     __shared__ int32_t ids[kAttnMaxSplitPages];
-    // a K2 launch over another layer may start early behind this one (PDL)
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // PDL: wait for the previous kernel (its block-table writes), then let
+    // the next launch (a K2 over another layer may start early) become resident
+    pdl_top();
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
@@ -730,8 +731,8 @@ size_t attention_tma_smem(int d, int G) {
 void launch_attention_tma(int d, dim3 grid, size_t smem, cudaStream_t st, const DevState& s, const AttnArgs& a,
                           const void* tmap) {
     const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap);
-    if (d == 128) attention_tma_kernel<128><<<grid, kAttnThreads, smem, st>>>(s, a, tm);
-    else attention_tma_kernel<64><<<grid, kAttnThreads, smem, st>>>(s, a, tm);
+    if (d == 128) launch_pdl(attention_tma_kernel<128>, grid, dim3(kAttnThreads), smem, st, s, a, tm);
+    else launch_pdl(attention_tma_kernel<64>, grid, dim3(kAttnThreads), smem, st, s, a, tm);
 }
 
 const void* attention_tma_fn(int d) {

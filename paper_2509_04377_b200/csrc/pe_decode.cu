@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
                                                                  unsigned long long ticket_base, int epoch,
                                                                  int fast_ok) {
     __shared__ int sh_lid, sh_warp_cnt[kAppendThreads / 32], sh_prefix, sh_pop_base, sh_fast;
+    pdl_top();  // launched with PDL: the launch gap behind the previous kernel is hidden
 #ifdef PE_K0_TRACE
     unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int polls = 0;
@@ -376,12 +377,6 @@ __device__ __forceinline__ int publish_chunk(const DevState& s, int t, int y, in
     return 1;
 }
 
-// Programmatic dependent launch (PDL) controls: a launch made with
-// programmatic stream serialization may start while the previous kernel of
-// the stream still runs; griddepcontrol.wait blocks until that kernel has
-// completed and its memory is visible (a no-op for a normal launch).
-__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
 // evict_score_kernel (K2, recompute): grid (launch tables, chunks). CTA (y, c)
@@ -486,7 +481,7 @@ void launch_evict_score_t(dim3 grid, int threads, cudaStream_t st, const DevStat
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = early ? 1 : 0;
+    cfg.numAttrs = (early || pdl_enabled()) ? 1 : 0;  // a non-early launch waits at its top
     cudaLaunchKernelEx(&cfg, evict_score_kernel<SV, HOLES>, s, ts, ppc, scratch, tickets, vpage, victims, grid_last,
                        early ? 1 : 0);
 }
@@ -509,8 +504,8 @@ void launch_append(int blocks, cudaStream_t st, const DevState& s, const TableSe
                    const uint8_t* v, const int64_t* pos, unsigned long long* lb, unsigned long long* lbg,
                    LaunchCtl* ctl, int fast_ok,
                    unsigned long long ticket_base, int epoch) {
-    append_kernel<SV><<<blocks, kAppendThreads, 0, st>>>(s, ts, k, v, pos, lb, lbg, ctl, ticket_base, epoch,
-                                                           fast_ok);
+    launch_pdl(append_kernel<SV>, dim3(blocks), dim3(kAppendThreads), 0, st, s, ts, k, v, pos, lb, lbg, ctl,
+               ticket_base, epoch, fast_ok);
 }
 
 void launch_evict_score_any(int variant, dim3 grid, int threads, cudaStream_t st, const DevState& s,
@@ -598,6 +593,7 @@ __device__ __forceinline__ void cached_evict_regs(const DevState& s, int t, int 
 __global__ void __launch_bounds__(256) evict_cached_kernel(DevState s, TableSet ts, double* scratch,
                                                            int32_t* vpage, int32_t* victims,
                                                            unsigned long long grid_last) {
+    pdl_top();
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int y = blockIdx.x * 8 + wid;

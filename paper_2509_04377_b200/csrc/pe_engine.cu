@@ -872,8 +872,8 @@ pe_status launch_evict(pe_engine* e, const DevState& sc, const TableSet& ts, int
                                e->evict_scratch, e->tickets, e->vpage, vdst, e->grid_tickets - 1, early);
     } else {
         e->grid_tickets += (unsigned long long)n;
-        evict_cached_kernel<<<(n + 7) / 8, 256, 0, st>>>(sc, ts, e->evict_scratch, e->vpage, vdst,
-                                                           e->grid_tickets - 1);
+        launch_pdl(evict_cached_kernel, dim3((n + 7) / 8), dim3(256), 0, st, sc, ts, e->evict_scratch, e->vpage,
+                   vdst, e->grid_tickets - 1);
     }
     pe_status r = check_launch(e, "evict kernel");
     if (r != PE_OK) return r;

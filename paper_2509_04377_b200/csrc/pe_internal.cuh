@@ -227,4 +227,18 @@ __device__ __forceinline__ void push_victims_if_last(const DevState& s, int n, i
     if (threadIdx.x == 0) *s.top = top + base;
 }
 
+// Programmatic dependent launch (PDL). A kernel launched with programmatic
+// stream serialization may become resident while the previous kernel of the
+// stream still runs; griddepcontrol.wait blocks until that kernel has
+// completed and its memory is visible (a no-op for a normal launch), and
+// griddepcontrol.launch_dependents lets the next PDL launch become resident.
+// Kernels that start with pdl_top() behave exactly like normally ordered
+// launches; PDL only hides the launch gap between them.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_top() {
+    pdl_wait();
+    pdl_launch_dependents();
+}
+
 }  // namespace pe

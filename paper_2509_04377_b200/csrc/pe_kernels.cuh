@@ -2,6 +2,10 @@
 // host side of the engine.
 #pragma once
 
+#include <cstdlib>
+#include <cstring>
+#include <utility>
+
 #include "pe_internal.cuh"
 
 namespace pe {
@@ -184,5 +188,27 @@ __global__ void invariants_free_kernel(DevState s, int32_t* refs);
 __global__ void invariants_refs_kernel(DevState s, const int32_t* refs, unsigned long long* counters);
 __global__ void probe_read_kernel(const uint4* src, size_t n16, unsigned long long* sink);
 __global__ void probe_copy_kernel(const uint4* src, uint4* dst, size_t n16);
+
+// Launch with programmatic stream serialization (kernels that start with
+// pdl_top(), or K2's early path) unless PE_PDL=0.
+inline bool pdl_enabled() {
+    const char* v = std::getenv("PE_PDL");
+    return !(v != nullptr && std::strcmp(v, "0") == 0);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace pe

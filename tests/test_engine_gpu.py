@@ -266,8 +266,10 @@ def test_serving_order_evict_attend_interleaved(pdl, monkeypatch):
     writes only its own partials and output; the eviction of another layer's
     tables streams while it drains). Victims of every layer and the GQA
     outputs (bf16 tolerance 1e-3) against the oracle at every step; the whole
-    state bit-exact at the end."""
+    state bit-exact at the end. PE_PDL=0 also turns off the PDL launches of
+    K0, K2c and K3 (each waits at its top, so only the launch gap differs)."""
     monkeypatch.setenv("PE_K2_PDL", pdl)
+    monkeypatch.setenv("PE_PDL", pdl)
     rng = np.random.default_rng(5150)
     B, C, H, G, n_layers, S, d = 16, 512, 4, 4, 3, 8, 128
     lens = np.full(S, 1200)
