@@ -49,10 +49,12 @@ def check(eng, orc, what="", pages=True):
                 assert st["page_scores"][pid] == ost["page_scores"][pid], f"{what}page score {pid}"
 
 
-@pytest.fixture(params=["default", "global_fallback", "stream512", "smem", "stream", "cluster"])
+@pytest.fixture(params=["default", "global", "global_fallback", "stream512", "smem", "stream", "cluster"])
 def select_path(request, monkeypatch):
-    """Run prefill through every select kernel: the default GPU-wide select
-    (window / count / resolve / emit, pe_select.cu), its fallback forced for
+    """Run prefill through every select kernel: the default (for these small
+    calls, fewer tables than half the SMs: the shared-memory CTA select), the
+    GPU-wide select (window / count / resolve / emit, pe_select.cu; the
+    default for larger calls) forced with PE_SELECT=global, its fallback forced for
     every table (PE_SELECT=global_fallback), the 512-thread streamed
     CTA select, the shared-memory CTA select, the 1024-thread streamed
     select and the 8-CTA cluster select."""
@@ -135,7 +137,7 @@ def prefill_variant(request, monkeypatch):
     return request.param
 
 
-@pytest.mark.parametrize("sel", ["default", "global_fallback", "stream512", "smem"])
+@pytest.mark.parametrize("sel", ["default", "global", "global_fallback", "stream512", "smem"])
 @pytest.mark.parametrize("gen", [random_kv, grid_kv])
 def test_prefill_long_tables_windowed_select(gen, prefill_variant, sel, monkeypatch):
     """Tables of >= 8192 tokens take the sampled pivot window (the GPU-wide

@@ -25,10 +25,11 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 import paper_2509_04377_b200 as pe  # noqa: E402
 
-CONFIGS = {  # name: (seqs, L, kv_heads, d, C)
-    "cfg2": (32, 16384, 8, 128, 2048),
-    "cfg3": (64, 32768, 8, 128, 4096),
-    "cfg5w": (16, 131072, 8, 128, 4096),  # one prompt wave of cfg5
+CONFIGS = {  # name: (seqs, L, kv_heads, d, C, dtype)
+    "cfg1": (1, 4096, 8, 64, 1024, "f32"),
+    "cfg2": (32, 16384, 8, 128, 2048, "bf16"),
+    "cfg3": (64, 32768, 8, 128, 4096, "bf16"),
+    "cfg5w": (16, 131072, 8, 128, 4096, "bf16"),  # one prompt wave of cfg5
 }
 B = 16
 
@@ -39,7 +40,8 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--variant", action="append", required=True, help="name:VAR=val,VAR=val")
     args = ap.parse_args()
-    S, L, H, d, C = CONFIGS[args.config]
+    S, L, H, d, C, dt = CONFIGS[args.config]
+    tdt, pdt, elt = (torch.bfloat16, pe.DTYPE_BF16, 2) if dt == "bf16" else (torch.float32, pe.DTYPE_F32, 4)
     variants = []
     for v in args.variant:
         name, _, envs = v.partition(":")
@@ -47,15 +49,15 @@ def main():
     keys = sorted({k for _, e in variants for k in e})
     n_layers = args.rounds * len(variants)
     eng = pe.PagedEvictionEngine(
-        pe.EngineGeometry(n_seqs=S, n_layers=n_layers, n_kv_heads=H, head_dim=d, dtype=pe.DTYPE_BF16),
+        pe.EngineGeometry(n_seqs=S, n_layers=n_layers, n_kv_heads=H, head_dim=d, dtype=pdt),
         pe.PolicyConfig(cache_budget=C, page_size=B))
     gen = torch.Generator(device="cuda")
     gen.manual_seed(2509)
-    k = torch.empty((S * L, H, d), dtype=torch.bfloat16, device="cuda").normal_(generator=gen)
+    k = torch.empty((S * L, H, d), dtype=tdt, device="cuda").normal_(generator=gen)
     v = torch.empty_like(k).normal_(generator=gen)
     cu = np.arange(S + 1, dtype=np.int32) * L
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    row = 2 * d * 2
+    row = 2 * d * elt
     keep = min(L, C)
     alg = S * H * (L * row + keep * row + 4 * keep + 4 * math.ceil(keep / B))
     times = {n: [] for n, _ in variants}
