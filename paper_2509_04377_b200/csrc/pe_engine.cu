@@ -1025,10 +1025,11 @@ pe_status pe_paged_decode_attention(pe_engine* e, int32_t layer, const void* q, 
     e->n_pending = 0;
     pe_status r = as_device(e, q, (size_t)s.n_seqs * n_q_heads * head_bytes, st, &dq);
     if (r != PE_OK) return r;
-    // as few splits as fill the GPU once (2 CTAs per SM): a CTA's warps stream
-    // their pages without draining, so long CTAs beat extra waves (cfg3: one
-    // split per table 181 us vs three 191 us)
-    int splits = std::max(1, (e->sm_count * 2 + n_tab - 1) / n_tab);
+    // as many splits as fit in one wave of CTAs (2 per SM), rounding down: a
+    // CTA's warps stream their pages without draining, so long CTAs beat
+    // extra waves (cfg3: one split per table 181 us vs three 191 us; cfg2's
+    // 256 tables: one split 47 us vs two 53 us)
+    int splits = std::max(1, (e->sm_count * 2) / n_tab);
     if (const char* sv = std::getenv("PE_ATTN_SPLITS")) splits = std::max(1, std::atoi(sv));
     splits = std::min(splits, std::max(1, (s.max_pages + 3) / 4));
     const int pps = (s.max_pages + splits - 1) / splits;
