@@ -619,9 +619,15 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     // dominate there (cfg1, 8 tables of 4096 tokens: 0.077 vs 0.095 ms per
     // layer).
     const bool small_call = sel_env == nullptr && n_tab < e->sm_count / 2 && max_len <= kSelectCtaMaxLen;
+    // Calls whose tables are all at most kGselMinLen tokens take the 512-thread
+    // streamed CTA select: its per-table latency grows with the table length,
+    // the GPU-wide select's chain does not (cfg2, 16384-token tables: 0.509 vs
+    // 0.540 ms per layer; cfg3, 32768: 1.805 vs 1.772; cfg4's mixed lengths up
+    // to 64K: 1.899 vs 1.868 for the first prompt wave)
+    const bool short_call = sel_env == nullptr && max_len <= kGselMinLen;
     const bool gsel_fb = env_is(sel_env, "global_fallback");  // test knob: the fallback for every table
     const bool use_gsel = (sel_env == nullptr || env_is(sel_env, "global") || gsel_fb) && !small_call &&
-                          !env_is(std::getenv("PE_SELECT_LONG"), "cluster") && max_len <= kGselMaxLen;
+                          !short_call && !env_is(std::getenv("PE_SELECT_LONG"), "cluster") && max_len <= kGselMaxLen;
     if (env_is(sel_env, "stream512")) sel_env = nullptr;
     const bool force_cluster = env_is(sel_env, "cluster");
     const bool force_stream = env_is(sel_env, "stream");

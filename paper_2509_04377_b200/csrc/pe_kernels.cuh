@@ -62,6 +62,7 @@ constexpr int kGselCandCap = 8192;                  // candidates sorted in shar
 constexpr int kGselMaxChunks = 128;                 // tables up to 128 chunks (262144 tokens)
 constexpr int kGselMaxLen = kGselChunk * kGselMaxChunks;
 constexpr int kGselMaxTies = 1024;                  // keys equal to the threshold resolved in the resolve kernel
+constexpr int kGselMinLen = 16384;                  // calls with shorter tables only: the streamed CTA select
 struct GselArgs {
     uint2* win;                          // [tables] high-word window (inclusive)
     int32_t* cand_n;                     // [tables] candidates appended

@@ -30,7 +30,13 @@ CONFIGS = {  # name: (seqs, L, kv_heads, d, C, dtype)
     "cfg2": (32, 16384, 8, 128, 2048, "bf16"),
     "cfg3": (64, 32768, 8, 128, 4096, "bf16"),
     "cfg5w": (16, 131072, 8, 128, 4096, "bf16"),  # one prompt wave of cfg5
+    "cfg4h": (128, 0, 8, 128, 4096, "bf16"),  # the first prompt wave of cfg4 (lengths as bench_configs)
 }
+
+
+def cfg4_lengths():
+    rng = np.random.default_rng(20250904 + 4)
+    return np.exp(rng.uniform(np.log(1024), np.log(65536), 256)).astype(int)[:128]
 B = 16
 
 
@@ -53,13 +59,13 @@ def main():
         pe.PolicyConfig(cache_budget=C, page_size=B))
     gen = torch.Generator(device="cuda")
     gen.manual_seed(2509)
-    k = torch.empty((S * L, H, d), dtype=tdt, device="cuda").normal_(generator=gen)
+    lens = cfg4_lengths() if args.config == "cfg4h" else np.full(S, L)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    k = torch.empty((int(cu[-1]), H, d), dtype=tdt, device="cuda").normal_(generator=gen)
     v = torch.empty_like(k).normal_(generator=gen)
-    cu = np.arange(S + 1, dtype=np.int32) * L
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     row = 2 * d * elt
-    keep = min(L, C)
-    alg = S * H * (L * row + keep * row + 4 * keep + 4 * math.ceil(keep / B))
+    alg = H * sum(int(x) * row + min(int(x), C) * (row + 4) + 4 * math.ceil(min(int(x), C) / B) for x in lens)
     times = {n: [] for n, _ in variants}
     layer_of = {n: [] for n, _ in variants}
     stream = torch.cuda.current_stream()
