@@ -38,6 +38,8 @@ VARIANTS = {
     "default": ({}, SMALL),
     "short_prompts": ({}, SHORT),
     "cached_score": ({}, SMALL + ["1"]),
+    "select_global": ({"PE_SELECT": "global"}, SMALL),
+    "select_global_fallback": ({"PE_SELECT": "global_fallback", "PE_FB_GRID": "7"}, SMALL),
     "select_smem": ({"PE_SELECT": "smem"}, SMALL),
     "select_cluster": ({"PE_SELECT": "cluster"}, SMALL),
     "select_stream1024": ({"PE_SELECT": "stream"}, SMALL),
@@ -48,9 +50,9 @@ VARIANTS = {
 
 TOOL_VARIANTS = {
     "memcheck": list(VARIANTS),
-    "racecheck": ["default", "short_prompts", "select_smem", "select_stream1024", "select_cluster",
-                  "attn_splits4_cpasync"],
-    "synccheck": ["default", "short_prompts", "select_cluster", "attn_splits4_cpasync"],
+    "racecheck": ["default", "short_prompts", "select_global", "select_global_fallback", "select_smem",
+                  "select_stream1024", "select_cluster", "attn_splits4_cpasync"],
+    "synccheck": ["default", "short_prompts", "select_global", "select_cluster", "attn_splits4_cpasync"],
 }
 
 
