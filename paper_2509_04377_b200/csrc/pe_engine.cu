@@ -598,6 +598,15 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     a.layer = layer;
     a.score_tokens = kScoreTokensPerCta;
     if (const char* stk = std::getenv("PE_SCORE_TOKENS")) a.score_tokens = std::max(16, std::atoi(stk));  // tuning
+    {
+        // tables that keep every token are packed by the score kernel (its
+        // staged-key path, blocks aligned to pages); PE_PREFILL_DIRECT=0: by the copy
+        const char* sk = std::getenv("PE_SCORE_STAGED_KEYS");
+        const char* dv = std::getenv("PE_PREFILL_DIRECT");
+        a.direct_identity = a.score_tokens % s.B == 0 && (int64_t)a.score_tokens * H <= kScoreKeysMax &&
+                            !(sk != nullptr && std::strcmp(sk, "0") == 0) &&
+                            !(dv != nullptr && std::strcmp(dv, "0") == 0);
+    }
     // PE_SELECT=cluster forces the cluster kernel (tests exercise both paths)
     // Select kernels. Default: tables of up to kSelectCtaMaxLen tokens take the
     // 512-thread streamed CTA select (two CTAs per SM), longer ones the
@@ -659,7 +668,9 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     const char* fz = std::getenv("PE_PREFILL_FUSED");
     if (smem_capable && fz != nullptr && std::strcmp(fz, "1") == 0) {
         // one persistent launch: score units and per-table select+copy items,
-        // X(q) scheduled after S(q+1) (prefill_fused_kernel)
+        // X(q) scheduled after S(q+1) (prefill_fused_kernel); its copies pack
+        // every table
+        a.direct_identity = 0;
         int kUnitTokens = 1024;
         if (const char* ut = std::getenv("PE_UNIT_TOKENS")) kUnitTokens = std::max(16, std::atoi(ut));
         int64_t n_items = 0;

@@ -39,6 +39,7 @@ struct PrefillArgs {
     int32_t cluster_len_min;             // cluster select: tables this short or shorter are skipped
     int32_t cand_cap;                    // streamed select: candidate list capacity (shared memory)
     int32_t bits_cap;                    // streamed select: eviction bitmap capacity in positions (0 = none)
+    int32_t direct_identity;             // score kernel packs tables that keep every token (L <= C); copy skips them
 };
 
 __global__ void evict_cached_kernel(DevState s, TableSet ts, double* scratch, int32_t* vpage, int32_t* victims,

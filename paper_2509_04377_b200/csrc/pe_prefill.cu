@@ -98,11 +98,27 @@ __global__ void __launch_bounds__(kPrefillThreads) prefill_score_kernel(DevState
     const int64_t f_hi = (int64_t)tok_hi * H;
     const int64_t row0 = a.tab_tok0[sq * H] * H;  // first (token, head) row of the sequence
     const int64_t n_units = (f_hi - f_lo + 15) / 16;
+    // a sequence whose tables keep every token (L <= C, or a non-evicting
+    // policy) needs no select: its rows go straight into their pages here
+    // (position p -> slot p % B of the table's (p / B)-th page), so they are
+    // read once instead of twice; the copy kernel skips these tables
+    const bool ident = SK && a.direct_identity &&
+                       !(s.policy == PE_POLICY_PAGED_EVICTION && L > s.C);  // block-uniform
+    const int B = s.B;
     for (int64_t u = wid; u < n_units; u += nw) {
         const int64_t f = f_lo + u * 16 + (lane >> 1);
         const bool valid = f < f_hi;
         const int64_t off = (row0 + f) * s.row_bytes;
-        const double S = pair_token_score<SV>(a.k + off, a.v + off, valid, s.w, s.dtype);
+        uint8_t* kd = nullptr;
+        uint8_t* vd = nullptr;
+        if (ident && valid) {
+            const int tok = static_cast<int>(f / H);
+            const int h = static_cast<int>(f - (int64_t)tok * H);
+            const int page = s.stack[ctl->pop_base - 1 - (a.tab_pagebase[sq * H + h] + tok / B)];
+            kd = s.pages + (((int64_t)page * 2 + 0) * B + tok % B) * s.pitch;
+            vd = s.pages + (((int64_t)page * 2 + 1) * B + tok % B) * s.pitch;
+        }
+        const double S = pair_token_score<SV>(a.k + off, a.v + off, valid, s.w, s.dtype, kd, vd);
         if (valid && (lane & 1) == 0) {
             const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(S));
             if constexpr (SK) {
@@ -120,6 +136,29 @@ __global__ void __launch_bounds__(kPrefillThreads) prefill_score_kernel(DevState
         for (int x = threadIdx.x; x < nt * H; x += blockDim.x) {  // head-major: one run per table
             const int h = x / nt, j = x - h * nt;
             a.keys[a.tab_keybase[sq * H + h] + tok_lo + j] = skeys[j * H + h];
+        }
+        if (ident) {
+            // positions and cached token scores of the packed slots, and the
+            // mean of every full page (slot-order sum / B, importance.cpp:19-30;
+            // the block starts on a page boundary: score_tokens % B == 0)
+            const int32_t* stk = s.stack + ctl->pop_base - 1;
+            for (int x = threadIdx.x; x < nt * H; x += blockDim.x) {
+                const int h = x / nt, j = x - h * nt;
+                const int tok = tok_lo + j;
+                const int page = stk[-(a.tab_pagebase[sq * H + h] + tok / B)];
+                s.positions[(int64_t)page * B + tok % B] = tok;
+                s.token_scores[(int64_t)page * B + tok % B] = __longlong_as_double(static_cast<long long>(skeys[j * H + h]));
+            }
+            const int pages_here = (nt + B - 1) / B;
+            for (int x = threadIdx.x; x < pages_here * H; x += blockDim.x) {
+                const int h = x / pages_here, pj = x - h * pages_here;
+                if (tok_lo + (pj + 1) * B > L) continue;  // the newest, partial page has no cached mean
+                double sum = 0.0;
+                for (int sl = 0; sl < B; ++sl)
+                    sum += __longlong_as_double(static_cast<long long>(skeys[(pj * B + sl) * H + h]));
+                const int page = stk[-(a.tab_pagebase[sq * H + h] + tok_lo / B + pj)];
+                s.page_scores[page] = sum / static_cast<double>(B);
+            }
         }
     }
 }
@@ -950,6 +989,7 @@ __device__ __forceinline__ void copy_page_warp(const DevState& s, const PrefillA
     const int lane = threadIdx.x & 31;
     const int L = a.tab_len[i];
     const int keep = (s.policy == PE_POLICY_PAGED_EVICTION && L > s.C) ? s.C : L;
+    if (a.direct_identity && keep == L) return;  // packed by the score kernel
     const int B = s.B;
     const int n_pages = (keep + B - 1) / B;
     if (j >= n_pages) return;
@@ -1012,6 +1052,7 @@ __global__ void __launch_bounds__(128) prefill_copy_score_kernel(DevState s, Pre
     const int lane = threadIdx.x & 31;
     const int L = a.tab_len[i];
     const int keep = (s.policy == PE_POLICY_PAGED_EVICTION && L > s.C) ? s.C : L;
+    if (a.direct_identity && keep == L) return;  // packed by the score kernel
     const int B = s.B;
     const int n_pages = (keep + B - 1) / B;
     if (j >= n_pages) return;

@@ -84,7 +84,7 @@ def test_prefill_parity(dtype, gen, select_path):
     check(eng, orc, "prefill: ")
 
 
-@pytest.mark.parametrize("variant", ["copy_gather", "unstaged_keys", "fallback_grid2"])
+@pytest.mark.parametrize("variant", ["copy_gather", "unstaged_keys", "fallback_grid2", "identity_by_copy"])
 @pytest.mark.parametrize("dtype", [oracle.F32, oracle.BF16])
 @pytest.mark.parametrize("gen", [random_kv, grid_kv])
 def test_prefill_kernel_variants(variant, dtype, gen, monkeypatch):
@@ -92,10 +92,13 @@ def test_prefill_kernel_variants(variant, dtype, gen, monkeypatch):
     survivor's key instead of rescoring its row (PE_COPY_RESCORE=0), per-warp
     key stores instead of the CTA-staged runs (PE_SCORE_STAGED_KEYS=0), and
     the global select's fallback looping over a wave's flagged tables with 2
-    CTAs (PE_FB_GRID=2, every table flagged). Bit-exact against the oracle."""
+    CTAs (PE_FB_GRID=2, every table flagged), and tables that keep every
+    token (L <= C) packed by the copy kernel instead of by the score kernel
+    (PE_PREFILL_DIRECT=0). Bit-exact against the oracle."""
     env = {"copy_gather": {"PE_COPY_RESCORE": "0"},
            "unstaged_keys": {"PE_SCORE_STAGED_KEYS": "0"},
-           "fallback_grid2": {"PE_FB_GRID": "2", "PE_SELECT": "global_fallback"}}[variant]
+           "fallback_grid2": {"PE_FB_GRID": "2", "PE_SELECT": "global_fallback"},
+           "identity_by_copy": {"PE_PREFILL_DIRECT": "0"}}[variant]
     monkeypatch.delenv("PE_SELECT", raising=False)
     for k_, v_ in env.items():
         monkeypatch.setenv(k_, v_)
