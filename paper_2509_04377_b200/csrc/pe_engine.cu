@@ -737,12 +737,47 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     // select's y (tables of a wave) are at most 65535
     waves = std::max(waves, (n_seqs + 65534) / 65535);
     if (any_long && long_cluster) waves = std::max(waves, (n_tab + 65534) / 65535);
+    const int max_keep_pages = (std::min(max_len, s.policy == PE_POLICY_PAGED_EVICTION ? s.C : max_len) + s.B - 1) / s.B;
+    const bool chain = env_is(std::getenv("PE_PREFILL_CHAIN"), "1");
+    // Mixed lengths: a compact score grid over the non-empty (sequence,
+    // token block) pairs instead of max_len/T blocks for every sequence (cfg4:
+    // most of the 2-D grid's CTAs would exit at once). Items are built on the
+    // host in sequence order, so wave w's items are one contiguous range.
+    const int max_blocks = (max_len + a.score_tokens - 1) / a.score_tokens;
+    std::vector<int> item_start;
+    {
+        int64_t n_items = 0;
+        for (int q = 0; q < n_seqs; ++q)
+            n_items += (cu_seqlens[q + 1] - cu_seqlens[q] + a.score_tokens - 1) / a.score_tokens;
+        const char* cg = std::getenv("PE_SCORE_COMPACT");  // A/B: 0 = always the 2-D grid
+        const bool compact = !(cg != nullptr && std::strcmp(cg, "0") == 0) && n_seqs <= 32767 &&
+                             max_blocks <= 0xFFFF && n_items < (int64_t)n_seqs * max_blocks * 4 / 5;
+        if (compact) {
+            if ((size_t)n_items > e->h_items_elems) {
+                if (e->h_items) PE_CUDA(cudaFreeHost(e->h_items));
+                e->h_items = nullptr;
+                e->h_items_elems = 0;
+                PE_CUDA(cudaMallocHost(&e->h_items, sizeof(int32_t) * n_items));
+                e->h_items_elems = (size_t)n_items;
+            }
+            if ((r = ensure_t(&e->items, &e->items_elems, (size_t)n_items)) != PE_OK) return r;
+            item_start.resize(n_seqs + 1);
+            int64_t k = 0;
+            for (int q = 0; q < n_seqs; ++q) {
+                item_start[q] = (int)k;
+                const int nb = (cu_seqlens[q + 1] - cu_seqlens[q] + a.score_tokens - 1) / a.score_tokens;
+                for (int b = 0; b < nb; ++b) e->h_items[k++] = (q << 16) | b;
+            }
+            item_start[n_seqs] = (int)k;
+            PE_CUDA(cudaMemcpyAsync(e->items, e->h_items, sizeof(int32_t) * n_items, cudaMemcpyHostToDevice, st));
+            PE_CUDA(cudaEventRecord(e->ev_meta, st));  // the next call rewrites h_items after this copy
+        }
+    }
+    // the aux stream's waves start after everything above on the caller's stream
     if (waves > 1) {
         PE_CUDA(cudaEventRecord(e->ev_fork, st));
         PE_CUDA(cudaStreamWaitEvent(e->aux_stream, e->ev_fork, 0));
     }
-    const int max_keep_pages = (std::min(max_len, s.policy == PE_POLICY_PAGED_EVICTION ? s.C : max_len) + s.B - 1) / s.B;
-    const bool chain = env_is(std::getenv("PE_PREFILL_CHAIN"), "1");
     GselArgs gs{};
     if (use_gsel) {
         gs.cand_stride = std::min(kGselCandCap, max_len);
@@ -779,8 +814,13 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
         // chained waves: this wave's score starts when the previous wave's
         // score is done, so that wave's select and copy run beside this score
         if (chain && w > 0) PE_CUDA(cudaStreamWaitEvent(sw, e->ev_score, 0));
-        launch_prefill_score_any(e->variant, dim3((max_len + aw.score_tokens - 1) / aw.score_tokens, q1 - q0),
-                                 sw, s, aw, e->ctl);
+        if (!item_start.empty()) {
+            aw.score_items = e->items + item_start[q0];
+            aw.item_seq0 = q0;
+            launch_prefill_score_any(e->variant, dim3(item_start[q1] - item_start[q0]), sw, s, aw, e->ctl);
+        } else {
+            launch_prefill_score_any(e->variant, dim3(max_blocks, q1 - q0), sw, s, aw, e->ctl);
+        }
         if (chain && w + 1 < waves) PE_CUDA(cudaEventRecord(e->ev_score, sw));
         if (use_gsel) {
             GselArgs gw = gs;

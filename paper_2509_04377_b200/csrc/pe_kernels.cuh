@@ -40,6 +40,8 @@ struct PrefillArgs {
     int32_t cand_cap;                    // streamed select: candidate list capacity (shared memory)
     int32_t bits_cap;                    // streamed select: eviction bitmap capacity in positions (0 = none)
     int32_t direct_identity;             // score kernel packs tables that keep every token (L <= C); copy skips them
+    const int32_t* score_items;          // compact score grid: (sequence << 16 | token block) per CTA, or nullptr
+    int32_t item_seq0;                   // sequence index (in the call) of the launch's first sequence
 };
 
 __global__ void evict_cached_kernel(DevState s, TableSet ts, double* scratch, int32_t* vpage, int32_t* victims,

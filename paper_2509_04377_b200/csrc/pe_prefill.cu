@@ -85,13 +85,20 @@ __global__ void __launch_bounds__(kPrefillThreads) prefill_score_kernel(DevState
                                                                          const LaunchCtl* ctl) {
     __shared__ unsigned long long skeys[SK ? kScoreKeysMax : 1];
     if (ctl->abort) return;
-    const int sq = blockIdx.y;  // sequence within the launch
+    // 2-D grid (token block, sequence), or a compact 1-D grid over the
+    // non-empty blocks of a call with mixed lengths (a.score_items)
+    int sq = blockIdx.y, bx = blockIdx.x;  // sequence within the launch, token block
+    if (a.score_items != nullptr) {
+        const int d = __ldg(a.score_items + blockIdx.x);
+        sq = (d >> 16) - a.item_seq0;
+        bx = d & 0xFFFF;
+    }
     const int H = s.tab_heads;
     const int L = a.tab_len[sq * H];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
-    const int tok_lo = blockIdx.x * a.score_tokens;
+    const int tok_lo = bx * a.score_tokens;
     if (tok_lo >= L) return;
     const int tok_hi = min(L, tok_lo + a.score_tokens);
     const int64_t f_lo = (int64_t)tok_lo * H;

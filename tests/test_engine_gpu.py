@@ -84,7 +84,8 @@ def test_prefill_parity(dtype, gen, select_path):
     check(eng, orc, "prefill: ")
 
 
-@pytest.mark.parametrize("variant", ["copy_gather", "unstaged_keys", "fallback_grid2", "identity_by_copy"])
+@pytest.mark.parametrize("variant", ["copy_gather", "unstaged_keys", "fallback_grid2", "identity_by_copy",
+                                     "score_grid_2d"])
 @pytest.mark.parametrize("dtype", [oracle.F32, oracle.BF16])
 @pytest.mark.parametrize("gen", [random_kv, grid_kv])
 def test_prefill_kernel_variants(variant, dtype, gen, monkeypatch):
@@ -94,11 +95,14 @@ def test_prefill_kernel_variants(variant, dtype, gen, monkeypatch):
     the global select's fallback looping over a wave's flagged tables with 2
     CTAs (PE_FB_GRID=2, every table flagged), and tables that keep every
     token (L <= C) packed by the copy kernel instead of by the score kernel
-    (PE_PREFILL_DIRECT=0). Bit-exact against the oracle."""
+    (PE_PREFILL_DIRECT=0), and the score kernel on its full 2-D grid instead
+    of the compact grid over non-empty blocks (PE_SCORE_COMPACT=0).
+    Bit-exact against the oracle."""
     env = {"copy_gather": {"PE_COPY_RESCORE": "0"},
            "unstaged_keys": {"PE_SCORE_STAGED_KEYS": "0"},
            "fallback_grid2": {"PE_FB_GRID": "2", "PE_SELECT": "global_fallback"},
-           "identity_by_copy": {"PE_PREFILL_DIRECT": "0"}}[variant]
+           "identity_by_copy": {"PE_PREFILL_DIRECT": "0"},
+           "score_grid_2d": {"PE_SCORE_COMPACT": "0"}}[variant]
     monkeypatch.delenv("PE_SELECT", raising=False)
     for k_, v_ in env.items():
         monkeypatch.setenv(k_, v_)
