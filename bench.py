@@ -25,9 +25,11 @@ prefill prune+pack of every layer from synthetic N(0,1) K/V.
 One bench STEP = one eviction cycle of the whole batch: B=16 decode tokens
 appended to every table (K0, one launch per token over all layers) followed
 by the PagedEviction block eviction of every table (K2, pages rescored from
-their resident K/V bytes; ONE launch covering all layers by default — each
-table's decision depends only on that table — `--evict-launch layer` runs
-one launch per layer; the other granularity is reported too). `value` =
+their resident K/V bytes; by default one launch per layer, issued back to
+back as a serving loop does, consecutive launches overlapping through
+programmatic dependent launch; `--evict-launch step` runs ONE launch
+covering all layers — each table's decision depends only on that table; the
+other granularity is reported too). `value` =
 algorithmic bytes of the step, summed over ranks (K2: (C+B)*row + 8*(C/B+1)
 + 4 per table; K0: 2*row+4 per table per token) / the max over ranks of the
 step's device time.
@@ -426,7 +428,9 @@ def run_b200(args, cfg, world, rank, local):
 
     # ---------------- decode inputs: B tokens of rows for every table (device + pinned host)
     # every decode token's positions, precomputed (no per-token increment kernel)
-    max_tokens = B * (2 * args.steps + args.warmup + 24 + max(0, 100 - args.steps))
+    # cycles that append: warm-up W + timed K + p50 extras max(0, 100 - K) + 4
+    # cached + 2 other-granularity + 2 x (1 + K) e2e + 2 decode (+ margin)
+    max_tokens = B * (args.warmup + 3 * max(1, args.steps) + max(0, 100 - args.steps) + 16)
     pos_all = (L + torch.arange(max_tokens, device=dev, dtype=torch.int64)).unsqueeze(1).expand(
         max_tokens, S).contiguous()
     tok = [0]
@@ -570,9 +574,10 @@ def run_b200(args, cfg, world, rank, local):
         q = torch.randn((S, QH, d), generator=gen, device=dev, dtype=torch.float32).to(tdt)
         out = torch.empty((S, QH, d), dtype=torch.float32, device=dev)
 
-        def decode_tokens(mode, attn_ms=None):
+        def decode_tokens(mode):
             """B decode tokens: per token K0 over all layers, then per layer the
-            trigger's eviction (on the B-th token) and K3."""
+            trigger's eviction (on the B-th token) and K3; no events between
+            launches (consecutive launches overlap through PDL, as in serving)."""
             barrier()
             d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             d0.record(stream)
@@ -581,23 +586,26 @@ def run_b200(args, cfg, world, rank, local):
                 for layer in range(NL):
                     if j == B - 1:
                         eng.evict(layer, 1, mode=mode)
-                    if attn_ms is not None:
-                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                        a.record(stream)
-                        eng.attend(layer, q, out, QH)
-                        b.record(stream)
-                        attn_ms.append((a, b))
-                    else:
-                        eng.attend(layer, q, out, QH)
+                    eng.attend(layer, q, out, QH)
             d1.record(stream)
             d1.synchronize()
             cycles[0] += 1
             return max_over_ranks(d0.elapsed_time(d1))
 
-        attn_ms = []
-        dec_ms = decode_tokens(pe.ScoreMode.RECOMPUTE, attn_ms)
+        dec_ms = decode_tokens(pe.ScoreMode.RECOMPUTE)
         dec_ms_c = decode_tokens(pe.ScoreMode.CACHED)
-        at = [a.elapsed_time(b) for a, b in attn_ms]
+        # K3 alone: every layer's attention back to back, one event pair per
+        # pass over the layers (per-layer time = pass / NL), 8 passes
+        attn_ms = []
+        for _ in range(8):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for layer in range(NL):
+                eng.attend(layer, q, out, QH)
+            b.record(stream)
+            attn_ms.append((a, b))
+        torch.cuda.synchronize()
+        at = [a.elapsed_time(b) / NL for a, b in attn_ms]
         k3_bytes = n_tab_layer * k3_bytes_per_table(C + B // 2, row, G, d, elt)
         decode = {"tokens_per_s": round(total_seqs * B / (dec_ms * 1e-3), 1),
                   "ms_per_token_all_layers": round(dec_ms / B, 4),
@@ -760,8 +768,9 @@ def main():
     ap.add_argument("--ref-tables", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
-    ap.add_argument("--evict-launch", default="step", choices=["layer", "step"],
-                    help="one K2 launch per layer, or one per decode step covering all layers")
+    ap.add_argument("--evict-launch", default="layer", choices=["layer", "step"],
+                    help="one K2 launch per layer (default: the serving granularity; consecutive launches "
+                         "overlap through PDL), or one per decode step covering all layers")
     ap.add_argument("--share-device", action="store_true",
                     help="test only: every rank on device 0 with the gloo backend")
     args = ap.parse_args()
