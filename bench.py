@@ -477,8 +477,13 @@ def run_b200(args, cfg, world, rank, local):
                 torch.cuda._sleep(200_000)
             a.record(stream)
         for l0, nl in spans:
-            vh = victims_host[l0 * n_tab_layer: (l0 + nl) * n_tab_layer] if victims_host is not None else None
-            eng.evict(l0, nl, step=0, mode=mode, victims=vh)
+            # e2e: every launch writes its victims into the step's device
+            # buffer, read back to host ONCE per step below (a serving loop
+            # reads the step's decisions, not one small copy per layer)
+            vd = vict_dev[l0 * n_tab_layer: (l0 + nl) * n_tab_layer] if victims_host is not None else None
+            eng.evict(l0, nl, step=0, mode=mode, victims=vd)
+        if victims_host is not None:
+            victims_host.copy_(vict_dev, non_blocking=True)
         if record is not None:
             b.record(stream)
             record.append((a, b, len(spans)))
@@ -540,6 +545,7 @@ def run_b200(args, cfg, world, rank, local):
 
     # ---------------- e2e: host buffers through the C-ABI (recompute, then cached scores)
     vict_host = torch.zeros(n_tab, dtype=torch.int32).pin_memory()  # step result read back
+    vict_dev = torch.zeros(n_tab, dtype=torch.int32, device=dev)
 
     def e2e_run(mode):
         cycle(host=True, victims_host=vict_host, mode=mode)  # warm the host-staging ring (untimed)
