@@ -596,7 +596,10 @@ pe_status pe_prefill_prune_pack(pe_engine* e, int32_t layer, const void* k, cons
     a.n_tab = n_tab;
     a.seq_begin = seq_begin;
     a.layer = layer;
-    a.score_tokens = kScoreTokensPerCta;
+    // tokens (x all heads) per score CTA: 128 while the CTA's keys fit the
+    // staged-key buffer (cfg3 1.827 -> 1.792 ms, cfg2 0.524 -> 0.518 against
+    // 64 tokens), else 64
+    a.score_tokens = (int64_t)kScoreTokensPerCta * H <= kScoreKeysMax ? kScoreTokensPerCta : 64;
     if (const char* stk = std::getenv("PE_SCORE_TOKENS")) a.score_tokens = std::max(16, std::atoi(stk));  // tuning
     {
         // tables that keep every token are packed by the score kernel (its

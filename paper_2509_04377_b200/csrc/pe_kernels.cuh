@@ -15,7 +15,7 @@ constexpr int kAppendEpochPeriod = 0x3FFFFFFE;  // K0 epochs 1..period: even, so
 constexpr int kEvictThreads = 128;       // 4 warps per CTA
 constexpr int kMaxPagesPerCta = 288;
 constexpr int kPrefillThreads = 128;     // score kernel: 4 warps per CTA
-constexpr int kScoreTokensPerCta = 64;   // tokens (x all heads) per score CTA (small CTAs balance best)
+constexpr int kScoreTokensPerCta = 128;  // tokens (x all heads) per score CTA (64 when the keys would not fit)
 constexpr int kScoreKeysMax = 1024;      // score CTA: keys staged in shared memory (8 KB)
 constexpr int kPackThreads = 256;        // select kernel: 8 warps per CTA
 constexpr int kPrefillCluster = 8;       // CTAs per table (portable cluster size)
