@@ -1052,7 +1052,7 @@ __global__ void __launch_bounds__(128) prefill_copy_kernel(DevState s, PrefillAr
 // row is issued before its stores, and no key is gathered): the score is the
 // same function of the same bytes, so it is bit-identical to the key.
 template <int SV>
-__global__ void __launch_bounds__(128) prefill_copy_score_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
+__global__ void __launch_bounds__(256) prefill_copy_score_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl) {
     if (ctl->abort) return;
     const int i = blockIdx.x;
     const int j = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1093,7 +1093,12 @@ void launch_prefill_copy_any(int variant, dim3 grid, cudaStream_t st, const DevS
     const char* rs = std::getenv("PE_COPY_RESCORE");  // A/B: 0 = gather the keys (prefill_copy_kernel)
     const bool rescore = !(rs != nullptr && std::strcmp(rs, "0") == 0) && s.pitch == s.row_bytes;
     if (rescore) {
-        PE_SCORE_DISPATCH(variant, (prefill_copy_score_kernel<SV><<<grid, 128, 0, st>>>(s, a, ctl)));
+        // one warp (destination page) per CTA: the gather balances best in
+        // small CTAs (cfg3 1.772 vs 1.785 ms with 4 warps, cfg2 0.511 vs 0.515)
+        const char* cw = std::getenv("PE_COPY_WARPS");  // A/B: warps (pages) per copy CTA
+        const int warps = cw ? std::max(1, std::min(8, std::atoi(cw))) : 1;
+        const dim3 g2(grid.x, (grid.y * 4 + warps - 1) / warps);
+        PE_SCORE_DISPATCH(variant, (prefill_copy_score_kernel<SV><<<g2, 32 * warps, 0, st>>>(s, a, ctl)));
     } else {
         prefill_copy_kernel<<<grid, 128, 0, st>>>(s, a, ctl);
     }
