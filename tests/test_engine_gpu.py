@@ -459,6 +459,53 @@ def test_attention_parity(dtype, tol):
                 assert dev_ <= tol, f"step {step} seq {s} head {hq}: deviation {dev_}"
 
 
+@pytest.mark.parametrize("B", [8, 32])
+@pytest.mark.parametrize("dtype", [oracle.F32, oracle.BF16])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_page_sizes_full_flow(B, dtype, mode):
+    """Page sizes other than 16 through the whole path: prefill (every select
+    path the call shape picks, tables below and above the budget, so the
+    score kernel's direct packing and the copy both run), decode cycles with
+    block evictions (recompute or cached scores) and attention (the CUDA-core
+    kernel: the tensor-core ones take B = 16 only). State bit-exact and
+    attention within tolerance against the oracle."""
+    rng = np.random.default_rng(3200 + B + dtype + 10 * mode)
+    C, H, G = 4 * B, 2, 2
+    d = 64 if dtype == oracle.F32 else 128
+    lens = np.array([C - 3, 7 * B + 5, C, 3 * C + 1, 2 * B])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=len(lens), n_layers=2, H=H, d=d, B=B, C=C, dtype=dtype)
+    for layer in range(2):
+        k, _ = random_kv(rng, (cu[-1], H, d), dtype)
+        v, _ = random_kv(rng, (cu[-1], H, d), dtype)
+        ev = eng.prefill_compress(layer, dev(k), dev(v), cu, evicted_counts=True)
+        st, oev = orc.prefill(layer, k, v, cu)
+        assert st == 0
+        np.testing.assert_array_equal(ev, oev)
+    pos = lens.astype(np.int64).copy()
+    tol = 1e-5 if dtype == oracle.F32 else 1e-3
+    for step in range(1, 2 * B + 3):
+        kk, _ = random_kv(rng, (2, len(lens), H, d), dtype)
+        vv, _ = random_kv(rng, (2, len(lens), H, d), dtype)
+        vic = eng.decode_step(0, 2, dev(kk), dev(vv), dev(pos), step, mode=mode, victims=True)
+        orc.decode_append(0, 2, kk, vv, pos)
+        _, ovic = orc.decode_evict(0, 2)
+        np.testing.assert_array_equal(vic, ovic, err_msg=f"step {step}")
+        pos += 1
+        if step % B == 0:
+            q, _ = random_kv(rng, (len(lens), H * G, d), dtype)
+            out = torch.empty((len(lens), H * G, d), dtype=torch.float32, device="cuda")
+            eng.attend(1, dev(q), out, H * G)
+            _, ref = orc.attention(1, q, G)
+            got = out.cpu().numpy()
+            for sq in range(len(lens)):
+                for hq in range(H * G):
+                    assert oracle.Oracle().output_deviation(got[sq, hq], ref[sq, hq]) <= tol
+    eng.sync()
+    check(eng, orc, f"B={B}: ")
+    assert eng.stats().pages_evicted > 0
+
+
 def test_host_buffers_match_device_buffers():
     rng = np.random.default_rng(3)
     B, C, d, H = 16, 64, 128, 2
