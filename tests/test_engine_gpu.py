@@ -506,6 +506,36 @@ def test_page_sizes_full_flow(B, dtype, mode):
     assert eng.stats().pages_evicted > 0
 
 
+@pytest.mark.parametrize("H", [16, 32])
+def test_prefill_many_kv_heads(H):
+    """More KV heads per sequence than the defaults plan for: 16 heads (score
+    CTAs of 64 tokens so the keys still fit the staging buffer) and 32 heads
+    (per-warp key stores, no direct packing of tables that keep every
+    token). Prefill and one eviction cycle bit-exact against the oracle."""
+    rng = np.random.default_rng(1600 + H)
+    B, C, d = 16, 64, 64
+    lens = np.array([C + 17, 40, 5 * C + 3, C])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    eng, orc = make_pair(n_seqs=len(lens), n_layers=1, H=H, d=d, B=B, C=C, dtype=oracle.BF16)
+    k, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+    v, _ = random_kv(rng, (cu[-1], H, d), oracle.BF16)
+    ev = eng.prefill_compress(0, dev(k), dev(v), cu, evicted_counts=True)
+    st, oev = orc.prefill(0, k, v, cu)
+    assert st == 0
+    np.testing.assert_array_equal(ev, oev)
+    pos = lens.astype(np.int64).copy()
+    for step in range(1, B + 1):
+        kk, _ = random_kv(rng, (1, len(lens), H, d), oracle.BF16)
+        vv, _ = random_kv(rng, (1, len(lens), H, d), oracle.BF16)
+        vic = eng.decode_step(0, 1, dev(kk), dev(vv), dev(pos), step, victims=True)
+        orc.decode_append(0, 1, kk, vv, pos)
+        _, ovic = orc.decode_evict(0, 1)
+        np.testing.assert_array_equal(vic, ovic, err_msg=f"step {step}")
+        pos += 1
+    eng.sync()
+    check(eng, orc, f"H={H}: ")
+
+
 def test_host_buffers_match_device_buffers():
     rng = np.random.default_rng(3)
     B, C, d, H = 16, 64, 128, 2
