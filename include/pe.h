@@ -43,6 +43,13 @@
  * word and make the failing launch a no-op; pe_sync() returns it.
  * Calls on one engine must be serialised by the caller (the reference's
  * BlockTable/EvictionPolicy are single-threaded, block_table.hpp:17-20).
+ * The decode-path kernels (append, evict, attention) are launched with
+ * programmatic dependent launch: each becomes resident behind the previous
+ * kernel of the stream and waits for it before it reads inputs or table
+ * state (plain stream-order semantics, without the launch gap); a per-layer
+ * evict that directly follows an evict or attention call over other layers
+ * of the same engine starts scoring early. Environment PE_PDL=0 /
+ * PE_K2_PDL=0 turn this off.
  */
 #ifndef PE_PE_H
 #define PE_PE_H
