@@ -583,17 +583,22 @@ __device__ __forceinline__ void cached_evict_regs(const DevState& s, int t, int 
         s.retained[t] -= page_fill(s, victim_page, s.B);
         if (s.holes_on) s.holes[victim_page] = 0ull;
         s.newest_fill[t] = (N - 1 > 0) ? s.B : 0;
-        vpage[y] = victim_page;
+        vpage[t] = victim_page;
         if (victims) victims[y] = victim;
         atomicAdd(s.evict_count, 1ull);
     }
     __syncwarp();
 }
 
+// early (PDL, per-layer launches back to back, as K2's): everything up to the
+// table's eviction touches only this launch's tables (vpage and scratch are
+// indexed by table id); the settle ticket and the push wait for the
+// previous launch.
 __global__ void __launch_bounds__(256) evict_cached_kernel(DevState s, TableSet ts, double* scratch,
                                                            int32_t* vpage, int32_t* victims,
-                                                           unsigned long long grid_last) {
-    pdl_top();
+                                                           unsigned long long grid_last, int early) {
+    if (!early) pdl_wait();
+    pdl_launch_dependents();
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int y = blockIdx.x * 8 + wid;
@@ -602,7 +607,7 @@ __global__ void __launch_bounds__(256) evict_cached_kernel(DevState s, TableSet 
         const int t = ts.table(s, y);
         if (!evict_triggered(s, t)) {
             if (lane == 0) {
-                vpage[y] = -1;
+                vpage[t] = -1;
                 if (victims) victims[y] = -1;
             }
         } else if (s.max_pages <= 32 * 9) {
@@ -612,13 +617,14 @@ __global__ void __launch_bounds__(256) evict_cached_kernel(DevState s, TableSet 
         } else {
             const int N = s.num_pages[t];
             const int32_t* row = s.block_table + (int64_t)t * s.max_pages;
-            double* sc = scratch + (int64_t)y * s.max_pages;
+            double* sc = scratch + (int64_t)t * s.max_pages;
             for (int j = lane; j < N; j += 32) sc[j] = s.page_scores[row[j]];
             __syncwarp();
-            finalize_evict(s, t, y, N, sc, vpage + y, victims);
+            finalize_evict(s, t, y, N, sc, vpage + t, victims);
         }
     }
-    push_victims_if_last(s, n, vpage, grid_last, min(8, n - static_cast<int>(blockIdx.x) * 8));
+    if (early) pdl_wait();  // the previous launch's settle tickets and pushes come first
+    push_victims_if_last(s, n, vpage, grid_last, min(8, n - static_cast<int>(blockIdx.x) * 8), &ts);
 }
 
 }  // namespace pe

@@ -912,7 +912,7 @@ pe_status launch_evict(pe_engine* e, const DevState& sc, const TableSet& ts, int
     // over a disjoint layer range of the same engine on the same stream
     // scores and evicts while that launch drains (evict_score_kernel `early`)
     const char* pdl_env = std::getenv("PE_K2_PDL");  // A/B: 0 = plain stream order
-    const bool early = mode == PE_SCORE_RECOMPUTE && !(pdl_env != nullptr && std::strcmp(pdl_env, "0") == 0) &&
+    const bool early = !(pdl_env != nullptr && std::strcmp(pdl_env, "0") == 0) &&
                        e->k2_chain && e->k2_stream == st && ts.ids == nullptr &&
                        (ts.layer_begin >= e->k2_layer0 + e->k2_layers ||
                         ts.layer_begin + ts.n_layers <= e->k2_layer0);
@@ -938,12 +938,22 @@ pe_status launch_evict(pe_engine* e, const DevState& sc, const TableSet& ts, int
                                e->evict_scratch, e->tickets, e->vpage, vdst, e->grid_tickets - 1, early);
     } else {
         e->grid_tickets += (unsigned long long)n;
-        launch_pdl(evict_cached_kernel, dim3((n + 7) / 8), dim3(256), 0, st, sc, ts, e->evict_scratch, e->vpage,
-                   vdst, e->grid_tickets - 1);
+        // PDL always (a non-early launch waits at its top); early: see K2
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((n + 7) / 8);
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = (early || pdl_enabled()) ? 1 : 0;
+        cudaLaunchKernelEx(&cfg, evict_cached_kernel, sc, ts, e->evict_scratch, e->vpage, vdst, e->grid_tickets - 1,
+                           early ? 1 : 0);
     }
     pe_status r = check_launch(e, "evict kernel");
     if (r != PE_OK) return r;
-    if (mode == PE_SCORE_RECOMPUTE && ts.ids == nullptr) {
+    if (ts.ids == nullptr) {  // either score mode: both touch only their own tables before the push
         e->k2_chain = true;
         e->k2_layer0 = ts.layer_begin;
         e->k2_layers = ts.n_layers;

@@ -45,7 +45,7 @@ struct PrefillArgs {
 };
 
 __global__ void evict_cached_kernel(DevState s, TableSet ts, double* scratch, int32_t* vpage, int32_t* victims,
-                                    unsigned long long grid_last);
+                                    unsigned long long grid_last, int early);
 __global__ void plan_prefill_kernel(DevState s, PrefillArgs a, int32_t total_pages, LaunchCtl* ctl);
 __global__ void prefill_select_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);
 __global__ void prefill_select_cta_kernel(DevState s, PrefillArgs a, const LaunchCtl* ctl);

@@ -227,8 +227,9 @@ def test_decode_parity(dtype, mode, k2, monkeypatch):
     assert eng.stats().pages_evicted > 0
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("pdl", ["1", "0"])
-def test_per_layer_evictions_back_to_back(pdl, monkeypatch):
+def test_per_layer_evictions_back_to_back(pdl, mode, monkeypatch):
     """Per-layer K2 launches issued back to back on one stream (a serving
     loop's eviction of every layer): with PE_K2_PDL=1 each launch after the
     first overlaps its predecessor (programmatic dependent launch: scoring
@@ -257,7 +258,10 @@ def test_per_layer_evictions_back_to_back(pdl, monkeypatch):
             pos += 1
         vics = [torch.full((S * H,), -7, dtype=torch.int32, device="cuda") for _ in range(n_layers)]
         for layer in range(n_layers):
-            eng.evict(layer, 1, step=(cycle + 1) * B, victims=vics[layer])
+            # alternate the score modes across layers in mode 1 (K2c and K2
+            # launches chained through PDL in both orders)
+            m = pe.ScoreMode.CACHED if (mode == 1 and (layer + cycle) % 2 == 0) else pe.ScoreMode.RECOMPUTE
+            eng.evict(layer, 1, step=(cycle + 1) * B, victims=vics[layer], mode=m)
         for layer in range(n_layers):
             _, ovic = orc.decode_evict(layer, 1)
             np.testing.assert_array_equal(vics[layer].cpu().numpy(), ovic, err_msg=f"cycle {cycle} layer {layer}")

@@ -23,7 +23,7 @@ if not lines:
 d = json.loads(lines[-1])
 p = d.get("prefill", {}); r = d.get("roofline", {})
 print(sys.argv[1].split("/")[-1], "value", d.get("value"), "k2_frac", r.get("frac"),
-      "p50_evict_us", d.get("p50_evict_step_us"), "layer_us", d.get("p50_evict_layer_launch_us"),
+      "p50_evict_step_us", d.get("p50_evict_step_us"), "launch_us", d.get("p50_evict_launch_us"),
       "append_us", d.get("append_us_per_launch_p50"),
       "prefill_ms", p.get("ms_per_layer_p50"), "prefill_frac", p.get("frac"),
       "checks", (d.get("checks") or {}).get("invariant_violations"), "clocks", d.get("clocks", {}).get("sm_mhz"))
