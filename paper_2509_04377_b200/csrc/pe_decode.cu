@@ -7,7 +7,19 @@
 #include "pe_score.cuh"
 
 #ifdef PE_K0_TRACE
-#include <cstdio>
+// Tooling build only (PE_NVCC_EXTRA=-DPE_K0_TRACE, tools/k0_trace.py):
+// %globaltimer stamps of thread 0 of the first kTraceCtas CTAs of the last
+// 64 append launches, read back with pe_debug_k0_trace.
+namespace pe {
+constexpr int kTraceCtas = 256, kTraceStamps = 10;
+__device__ unsigned long long g_k0_trace[64 * kTraceCtas * kTraceStamps];
+}  // namespace pe
+extern "C" int pe_debug_k0_trace(void* out, size_t bytes) {
+    return cudaMemcpyFromSymbol(out, pe::g_k0_trace, bytes < sizeof(pe::g_k0_trace) ? bytes : sizeof(pe::g_k0_trace)) ==
+                   cudaSuccess
+               ? 0
+               : -1;
+}
 #endif
 
 namespace pe {
@@ -56,15 +68,15 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
                                                                  unsigned long long ticket_base, int epoch,
                                                                  int fast_ok) {
     __shared__ int sh_lid, sh_warp_cnt[kAppendThreads / 32], sh_prefix, sh_pop_base, sh_fast;
-    pdl_top();  // launched with PDL: the launch gap behind the previous kernel is hidden
 #ifdef PE_K0_TRACE
-    unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int polls = 0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr[0]));
+    unsigned long long tr[kTraceStamps] = {};
 #define PE_TR(i) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr[i]))
 #else
 #define PE_TR(i)
 #endif
+    PE_TR(0);   // resident
+    pdl_top();  // launched with PDL: the launch gap behind the previous kernel is hidden
+    PE_TR(8);   // previous kernel complete
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = kAppendThreads / 32;
@@ -213,11 +225,6 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
     const double S = pair_token_score<SV>(k_rows + in_row * s.row_bytes, v_rows + in_row * s.row_bytes, served, s.w,
                                           s.dtype, served ? kdst : nullptr, served ? vdst : nullptr);
     PE_TR(5);
-#ifdef PE_K0_TRACE
-    if (threadIdx.x == 0 && epoch % 64 == 40)
-        printf("K0TRACE epoch %d lid %d t0 %llu t1 %llu t2 %llu walk %llu top %llu t3 %llu t4 %llu t5 %llu\n", epoch, lid,
-               tr[0], tr[1], tr[2], tr[6], tr[7], tr[3], tr[4], tr[5]);
-#endif
     if (served && q == 0) {
         const int64_t ps = (int64_t)page * s.B + slot;
         s.positions[ps] = static_cast<int32_t>(positions[ts.pos_index(s, my_i)]);
@@ -254,6 +261,13 @@ __global__ void __launch_bounds__(kAppendThreads) append_kernel(DevState s, Tabl
         const int next = epoch % kAppendEpochPeriod + 1;  // the next launch's epoch (opposite parity)
         *reinterpret_cast<volatile unsigned int*>(&ctl->pop_flag[next & 1]) = static_cast<unsigned>(next);
     }
+#ifdef PE_K0_TRACE
+    PE_TR(9);
+    if (threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
+        unsigned long long* o = g_k0_trace + ((int64_t)(epoch % 64) * kTraceCtas + blockIdx.x) * kTraceStamps;
+        for (int k = 0; k < kTraceStamps; ++k) o[k] = tr[k];
+    }
+#endif
     (void)nw;
 }
 
